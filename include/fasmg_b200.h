@@ -1,0 +1,150 @@
+/*
+ * fasmg_b200.h -- C ABI of libfasmg_b200.so, the B200 (sm_100a) native
+ * FAS multigrid path of arXiv 2510.11152.
+ *
+ * Two layers, matching the two reference interfaces that this library
+ * replaces:
+ *
+ *  (b1) the kernel ABI of the reference backend dispatcher
+ *       (/root/reference/pkg/src/fasmg/kernels/__init__.py:37-98): the 16
+ *       kernels by name, same argument order and meaning as
+ *       kernels/numpy_backend.py, on DEVICE arrays.  Every array argument is
+ *       (pointer to the core-view origin, int64 element strides[ndim]) --
+ *       the core view of PKG/grid.py:199-208 where array index equals grid
+ *       index.  Bounds are inclusive.  Kernels mutate in place.
+ *
+ *  (b2) the solver engine behind FasSolver (PKG/fas.py:63-181): create a
+ *       solver for one hierarchy/location/BC/plan/coefficients, load p and f,
+ *       run V-cycles (each optionally followed by the outer residual norm),
+ *       store p back.  The engine runs on its own parity-blocked layout and
+ *       replays the V-cycle as a CUDA graph.
+ *
+ * Conventions: every int-returning function returns 0 on success or a
+ * FASMG_E* code; fasmg_last_error() gives the message (thread-local).
+ * `stream` is a cudaStream_t (may be NULL only where noted).  No function
+ * synchronizes the device unless documented.  Not thread-safe per engine.
+ *
+ * BC encoding (PKG/boundary.py:22-87): kinds[6] / vals[6] in face order
+ * xlo, xhi, ylo, yhi, zlo, zhi; kind 0 = dirichlet (reflected; wall value on
+ * an edge axis), 1 = neumann (copy), 2 = periodic.  Edge axis `ea`: -1 for
+ * cell-centered, else 0/1/2 (Location.edge_axis, PKG/grid.py:37-41).
+ */
+#ifndef FASMG_B200_H
+#define FASMG_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FASMG_OK 0
+#define FASMG_EINVAL 1001
+#define FASMG_ECUDA 1002
+#define FASMG_ENOMEM 1003
+#define FASMG_ESTATE 1004
+
+/* ---- runtime ------------------------------------------------------------ */
+const char* fasmg_last_error(void);
+int fasmg_last_error_code(void);
+int fasmg_version(void);
+int fasmg_compiled_arch(void);
+int fasmg_device_count(int* n);
+int fasmg_stream_create(void** stream);
+int fasmg_stream_destroy(void* stream);
+int fasmg_stream_synchronize(void* stream);
+int fasmg_stream_wait(void* waiter, void* signaler);
+
+/* ---- (b1) kernel ABI: KER/__init__.py:37-46, KER/numpy_backend.py ------- */
+/* replaces gs_sweep_2d (KER/numpy_backend.py:27-44) */
+int fasmg_gs_sweep_2d(double* p, const long* ps, const double* f, const long* fs, double b,
+                      double h2, double denom, int ilo, int ihi, int jlo, int jhi, int ipar,
+                      int jpar, void* stream);
+/* replaces gs_sweep_3d (KER/numpy_backend.py:47-62) */
+int fasmg_gs_sweep_3d(double* p, const long* ps, const double* f, const long* fs, double b,
+                      double h2, double denom, int ilo, int ihi, int jlo, int jhi, int klo,
+                      int khi, int ipar, int jpar, int kpar, void* stream);
+/* replaces apply_op_2d / apply_op_3d (KER/numpy_backend.py:91-99) */
+int fasmg_apply_op_2d(double* out, const long* os, const double* p, const long* ps, double a,
+                      double b, double inv_h2, int ilo, int ihi, int jlo, int jhi, void* stream);
+int fasmg_apply_op_3d(double* out, const long* os, const double* p, const long* ps, double a,
+                      double b, double inv_h2, int ilo, int ihi, int jlo, int jhi, int klo,
+                      int khi, void* stream);
+/* replaces residual_2d / residual_3d (KER/numpy_backend.py:102-112) */
+int fasmg_residual_2d(double* out, const long* os, const double* p, const long* ps,
+                      const double* fsrc, const long* fs, double a, double b, double inv_h2,
+                      int ilo, int ihi, int jlo, int jhi, void* stream);
+int fasmg_residual_3d(double* out, const long* os, const double* p, const long* ps,
+                      const double* fsrc, const long* fs, double a, double b, double inv_h2,
+                      int ilo, int ihi, int jlo, int jhi, int klo, int khi, void* stream);
+/* replaces restrict_cc_2d/3d, prolong_cc_2d/3d (KER/numpy_backend.py:119-155) */
+int fasmg_restrict_cc_2d(const double* fine, const long* fs, double* coarse, const long* cs,
+                         int m0, int n0, void* stream);
+int fasmg_restrict_cc_3d(const double* fine, const long* fs, double* coarse, const long* cs,
+                         int m0, int n0, int l0, void* stream);
+int fasmg_prolong_cc_2d(const double* coarse, const long* cs, double* fine, const long* fs,
+                        int m0, int n0, void* stream);
+int fasmg_prolong_cc_3d(const double* coarse, const long* cs, double* fine, const long* fs,
+                        int m0, int n0, int l0, void* stream);
+/* replaces restrict_edge0_2d/3d, prolong_edge0_2d/3d (KER/numpy_backend.py:162-224);
+ * callers pass edge-axis-first permuted strides as PKG/transfer.py:41-45 does */
+int fasmg_restrict_edge0_2d(const double* fine, const long* fs, double* coarse,
+                            const long* cs, int m0, int n0, void* stream);
+int fasmg_restrict_edge0_3d(const double* fine, const long* fs, double* coarse,
+                            const long* cs, int m0, int n0, int l0, void* stream);
+int fasmg_prolong_edge0_2d(const double* coarse, const long* cs, double* fine,
+                           const long* fs, int m0, int n0, void* stream);
+int fasmg_prolong_edge0_3d(const double* coarse, const long* cs, double* fine,
+                           const long* fs, int m0, int n0, int l0, void* stream);
+/* replaces weno_deriv0_2d/3d (KER/numpy_backend.py:231-262); out and wind
+ * are interior-shaped (ni, nj[, nk]); q is the full array view */
+int fasmg_weno_deriv0_2d(double* out, const long* os, const double* q, const long* qs,
+                         const double* wind, const long* ws, int ni, int nj, int oi, int oj,
+                         double inv_2h, double eps, void* stream);
+int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const long* qs,
+                         const double* wind, const long* ws, int ni, int nj, int nk, int oi,
+                         int oj, int ok, double inv_2h, double eps, void* stream);
+
+/* ---- field-level helpers ------------------------------------------------ */
+/* replaces fill_ghosts (PKG/boundary.py:90-107) on a C-contiguous data array
+ * of a field with n[dim] cells, edge axis ea and halo `halo` */
+int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, const int* kinds,
+                      const double* vals, void* stream);
+/* np.sum of a (non-contiguous) interior view in numpy 2.3's buffered-reduce
+ * order, used by the mean projection (PKG/fas.py:145,156); out[0] on device.
+ * scratch >= prod(ext) doubles; sums >= fasmg_view_sum_chunks() doubles */
+int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, double* scratch,
+                   double* sums, double* out, void* stream);
+long fasmg_view_sum_chunks(int dim, const int* ext);
+/* v -= total[0] / count over an interior view */
+int fasmg_sub_mean(double* v, const long* vs, int dim, const int* ext, const double* total,
+                   double count, void* stream);
+
+/* ---- (b2) solver engine: FasSolver (PKG/fas.py:63-162) ------------------ */
+/* FasSolver.__init__ (PKG/fas.py:71-89): n[dim] finest cells, mesh_level
+ * coarsenings, operator a*p - b*Lap(p) (PKG/stencil.py:21-38), smoothing
+ * plan as class masks (bit c = parity class q0*4+q1*2+q2 in 3D, q0*2+q1 in
+ * 2D; one mask per ghost-refresh group of make_plan, PKG/smoothers.py:87),
+ * s smoothing steps per stage.  Returns NULL on error. */
+void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dmax,
+                          int mesh_level, double a, double b, const int* kinds,
+                          const double* vals, int nmasks, const unsigned* masks, int s,
+                          void* stream);
+void fasmg_engine_destroy(void* engine);
+/* copy p and f (core views, strides) into the engine (enqueued on the
+ * engine stream) */
+int fasmg_engine_load(void* engine, const double* pcore, const long* ps, const double* fcore,
+                      const long* fs);
+/* write the solution interior back into a core view */
+int fasmg_engine_store(void* engine, double* pcore, const long* ps);
+/* run `count` V-cycles (PKG/fas.py:96-128); with_norm adds the outer
+ * residual's sum of squares after each (PKG/fas.py:149-151) and returns the
+ * last one in *sumsq after synchronizing; use_graph replays a captured
+ * CUDA graph */
+int fasmg_engine_run(void* engine, int count, int with_norm, double* sumsq, int use_graph);
+int fasmg_engine_residual_sumsq(void* engine, double* sumsq);
+long fasmg_engine_kernels_per_vcycle(void* engine);
+int fasmg_engine_level_info(void* engine, int level, long* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASMG_B200_H */

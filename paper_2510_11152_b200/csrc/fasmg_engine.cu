@@ -1,0 +1,915 @@
+// fasmg_engine.cu -- the B200 FAS V-cycle on the parity-blocked layout.
+//
+// Layout.  A level with n_a cells per axis is stored as 2^d "class" arrays,
+// one per index-parity tuple q = (i&1, j&1[, k&1]).  Grid index x_a maps to
+// class bit q_a = x_a & 1 and block b_a = (x_a + 1) >> 1, so block b holds
+// the 2^d children (2b-1, 2b) of coarse cell b.  Each class array covers
+// blocks 0..B_a+1 (B_a = n_a/2) per axis, the last axis contiguous, padded
+// so block 1 of every row starts on a 32-byte boundary.
+//
+// Why: X-MCGS (PKG/smoothers.py:41-45, 136-153) updates one index-parity
+// class per color; the first four colors (odd index sum) never read each
+// other, nor do the last four, so one smoothing sweep is two dependent
+// half-sweeps.  In this layout a half-sweep
+// reads the 2^(d-1) opposite classes plus f of its own classes and writes
+// its classes: 12 B/DOF, 24 B/DOF per sweep -- the bandwidth minimum -- with
+// 256-byte coalesced warp accesses and no parity branching.  Restriction
+// and injection become same-index operations across the 2^d classes.
+//
+// Ghosts.  The reference refills ghosts before every color
+// (PKG/smoothers.py:149).  A 5/7-point stencil reads a ghost only through
+// the single axis it crosses, and that ghost mirrors either the updated
+// point itself (Dirichlet 2v - p, Neumann copy), the opposite-parity wrap
+// (periodic) or a prescribed wall value, so every kernel evaluates ghosts
+// inline from current values -- bitwise identical, no ghost-fill launches.
+// Edge-centered transfers, which read corner ghosts, use the full
+// fill-order chain (ghost_value in fasmg_common.cuh).
+//
+// Fusions (FAS V-cycle, PKG/fas.py:96-128):
+//  * residual + both cell restrictions + FAS tau source in one pass
+//    (tau kernel), the coarse operator L_2h(R p) added by a coarse kernel;
+//  * the coarse correction c = p_c - R(p) is formed on the fly from the
+//    unchanged fine p, so the reference's pinit copy is never stored;
+//  * outer residual + sum of squares fused (no residual array).
+// The whole V-cycle plus the residual norm is captured once as a CUDA
+// graph and replayed per outer iteration.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "fasmg_common.cuh"
+#include "fasmg_internal.h"
+
+namespace fasmg {
+
+static constexpr int OFF = 3;  // element offset so block 1 is 32B-aligned
+static constexpr int TPB = 256;
+
+struct Lvl {
+    int dim, ea;
+    int n[3], B[3], E[3];
+    long s0, s1, cls;  // strides of block axes 0,1 (last axis stride 1)
+    long nblk;         // interior blocks
+    double h, h2, inv_h2, denom, a, b;
+};
+
+template <int D>
+__device__ __forceinline__ long at(const Lvl& L, int c, int b0, int b1, int b2) {
+    if (D == 3) return c * L.cls + b0 * L.s0 + b1 * L.s1 + b2 + OFF;
+    return c * L.cls + b0 * L.s0 + b1 + OFF;
+}
+
+template <int D>
+__device__ __forceinline__ void decode(const Lvl& L, long t, int* bb) {
+    if (D == 3) {
+        bb[2] = 1 + (int)(t % L.B[2]);
+        long r = t / L.B[2];
+        bb[1] = 1 + (int)(r % L.B[1]);
+        bb[0] = 1 + (int)(r / L.B[1]);
+    } else {
+        bb[1] = 1 + (int)(t % L.B[1]);
+        bb[0] = 1 + (int)(t / L.B[1]);
+        bb[2] = 0;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ int qbit(int c, int axis) { return (c >> (D - 1 - axis)) & 1; }
+
+// is (class c, block bb) an interior point? (edge axis: class-0 block B is
+// the high wall)
+template <int D>
+__device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
+    if (L.ea < 0) return true;
+    return !(qbit<D>(c, L.ea) == 0 && bb[L.ea] == L.B[L.ea]);
+}
+
+// Neighbor of point (c, bb) along `axis` in direction dir (+1/-1), with
+// the reference's ghost semantics evaluated inline.  `self` is the current
+// value of the point itself (needed only by Dirichlet/Neumann ghosts).
+template <int D>
+__device__ __forceinline__ double nbr(const double* P, const Lvl& L, const BcSpec& bc, int c,
+                                      const int* bb, int axis, int dir, const double* selfp) {
+    const int bit = 1 << (D - 1 - axis);
+    const int q = (c & bit) ? 1 : 0;
+    const int cn = c ^ bit;
+    int nb[3] = {bb[0], bb[1], bb[2]};
+    const int bn = bb[axis] + (q ? (dir > 0 ? 0 : -1) : (dir > 0 ? 1 : 0));
+    const bool edge = (axis == L.ea);
+    const int hi = (q == 1 && edge) ? L.B[axis] - 1 : L.B[axis];  // qn = 1 - q
+    if (bn >= 1 && bn <= hi) {
+        nb[axis] = bn;
+        return P[at<D>(L, cn, nb[0], nb[1], nb[2])];
+    }
+    const int side = dir > 0 ? 1 : 0;
+    const int kind = bc.kind[axis][side];
+    const double v = bc.val[axis][side];
+    if (kind == BC_NEUMANN) return *selfp;
+    if (!edge) {
+        if (kind == BC_DIRICHLET) return sb(ml(2.0, v), *selfp);
+        nb[axis] = dir < 0 ? L.B[axis] : 1;  // periodic wrap, same class cn
+        return P[at<D>(L, cn, nb[0], nb[1], nb[2])];
+    }
+    if (kind == BC_DIRICHLET) return v;
+    nb[axis] = 0;  // periodic edge axis: both walls hold the stored low wall
+    return P[at<D>(L, cn, nb[0], nb[1], nb[2])];
+}
+
+template <int D>
+__device__ __forceinline__ double nsum_at(const double* P, const Lvl& L, const BcSpec& bc,
+                                          int c, const int* bb, const double* selfp) {
+    // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:58-62)
+    double s = ad(nbr<D>(P, L, bc, c, bb, 0, +1, selfp), nbr<D>(P, L, bc, c, bb, 0, -1, selfp));
+    s = ad(s, nbr<D>(P, L, bc, c, bb, 1, +1, selfp));
+    s = ad(s, nbr<D>(P, L, bc, c, bb, 1, -1, selfp));
+    if (D == 3) {
+        s = ad(s, nbr<D>(P, L, bc, c, bb, 2, +1, selfp));
+        s = ad(s, nbr<D>(P, L, bc, c, bb, 2, -1, selfp));
+    }
+    return s;
+}
+
+// ------------------------------------------------------------- smoothing
+// One launch updates every class in `mask` (classes that are mutually
+// independent: equal index-sum parity).  Thread per block.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_sweep(double* __restrict__ P,
+                                               const double* __restrict__ F, Lvl L,
+                                               BcSpec bc, unsigned mask) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+    double out[1 << D];
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (!(mask & (1u << c))) continue;
+        if (!interior<D>(L, c, bb)) continue;
+        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+        double ns = nsum_at<D>(P, L, bc, c, bb, P + o);
+        out[c] = dv(ad(ml(L.h2, F[o]), ml(L.b, ns)), L.denom);
+    }
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (!(mask & (1u << c))) continue;
+        if (!interior<D>(L, c, bb)) continue;
+        P[at<D>(L, c, bb[0], bb[1], bb[2])] = out[c];
+    }
+}
+
+// a*c - b*lap at one point (KER/numpy_backend.py:69-99)
+template <int D>
+__device__ __forceinline__ double op_at(const double* P, const Lvl& L, const BcSpec& bc, int c,
+                                        const int* bb, long o) {
+    const double cv = P[o];
+    double ns = nsum_at<D>(P, L, bc, c, bb, P + o);
+    double lap = ml(sb(ns, ml(D == 3 ? 6.0 : 4.0, cv)), L.inv_h2);
+    return sb(ml(L.a, cv), ml(L.b, lap));
+}
+
+// ----------------------------------------------------------- tau kernel
+// Cell-centered: residual at the 2^d children of coarse cell b, restriction
+// of r and p (lexicographic child order = descending class id,
+// KER/numba_backend.py:222-253), written to the coarse level's classes.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_tau_cell(const double* __restrict__ P,
+                                                  const double* __restrict__ F, Lvl L,
+                                                  BcSpec bc, double* __restrict__ Pc,
+                                                  double* __restrict__ Fc, Lvl Lc) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+    double rp = 0.0, rr = 0.0;
+#pragma unroll
+    for (int c = (1 << D) - 1; c >= 0; --c) {
+        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+        const double pv = P[o];
+        const double r = sb(F[o], op_at<D>(P, L, bc, c, bb, o));
+        if (c == (1 << D) - 1) { rp = pv; rr = r; }
+        else { rp = ad(rp, pv); rr = ad(rr, r); }
+    }
+    const double sc = D == 3 ? 0.125 : 0.25;
+    // coarse cell index I = bb -> coarse class (I&1), block (I+1)>>1
+    int cc = 0, cb[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        cc |= (bb[a] & 1) << (D - 1 - a);
+        cb[a] = (bb[a] + 1) >> 1;
+    }
+    const long oc = at<D>(Lc, cc, cb[0], cb[1], cb[2]);
+    Pc[oc] = ml(rp, sc);
+    Fc[oc] = ml(rr, sc);
+}
+
+// f_c += a*p_c - b*Lap(p_c) on the coarse level (PKG/fas.py:107-110): full
+// BC ghosts on p_c.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_coarse_src(const double* __restrict__ Pc,
+                                                    double* __restrict__ Fc, Lvl L, BcSpec bc) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (!interior<D>(L, c, bb)) continue;
+        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+        Fc[o] = ad(Fc[o], op_at<D>(Pc, L, bc, c, bb, o));
+    }
+}
+
+// Coarse correction, cell-centered (PKG/fas.py:119-123): c = p_c - R(p)
+// with R(p) recomputed from the unchanged fine p (equal to the stored
+// pinit), injected to the 2^d children and added.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_correct_cell(double* __restrict__ P, Lvl L,
+                                                      const double* __restrict__ Pc, Lvl Lc) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+    double pv[1 << D];
+    double rp = 0.0;
+#pragma unroll
+    for (int c = (1 << D) - 1; c >= 0; --c) {
+        pv[c] = P[at<D>(L, c, bb[0], bb[1], bb[2])];
+        rp = (c == (1 << D) - 1) ? pv[c] : ad(rp, pv[c]);
+    }
+    rp = ml(rp, D == 3 ? 0.125 : 0.25);
+    int cc = 0, cb[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        cc |= (bb[a] & 1) << (D - 1 - a);
+        cb[a] = (bb[a] + 1) >> 1;
+    }
+    const double corr = sb(Pc[at<D>(Lc, cc, cb[0], cb[1], cb[2])], rp);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) P[at<D>(L, c, bb[0], bb[1], bb[2])] = ad(pv[c], corr);
+}
+
+// ------------------------------------------------- edge-centered transfers
+// Residual into R (edge fields need it for the tangential stencil).
+template <int D>
+__global__ void __launch_bounds__(TPB) k_residual(const double* __restrict__ P,
+                                                  const double* __restrict__ F,
+                                                  double* __restrict__ R, Lvl L, BcSpec bc) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (!interior<D>(L, c, bb)) continue;
+        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+        R[o] = sb(F[o], op_at<D>(P, L, bc, c, bb, o));
+    }
+}
+
+// Reader of raw stored values at core (grid) index x in the blocked layout.
+template <int D>
+struct BlkReader {
+    const double* P;
+    Lvl L;
+    __device__ double operator()(int x0, int x1, int x2) const {
+        int x[3] = {x0, x1, x2};
+        int c = 0, b[3] = {0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            c |= (x[a] & 1) << (D - 1 - a);
+            b[a] = (x[a] + 1) >> 1;
+        }
+        return P[at<D>(L, c, b[0], b[1], b[2])];
+    }
+};
+
+template <int D>
+__device__ __forceinline__ double gval(const double* P, const Lvl& L, const BcSpec& bc, int x0,
+                                       int x1, int x2) {
+    AxisGeo ax[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        ax[a].m = a < D ? L.n[a] : 1;
+        ax[a].edge = (a == L.ea);
+    }
+    BlkReader<D> rd{P, L};
+    return ghost_value<D>(ax, bc, x0, x1, x2, rd);
+}
+
+// Fine value at grid index x with ghosts filled under bc: fast path for
+// interior points.
+template <int D>
+__device__ __forceinline__ double fval(const double* P, const Lvl& L, const BcSpec& bc,
+                                       const int* x) {
+    bool in = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        int hi = (a == L.ea) ? L.n[a] - 1 : L.n[a];
+        in = in && x[a] >= 1 && x[a] <= hi;
+    }
+    if (in) {
+        BlkReader<D> rd{P, L};
+        return rd(x[0], x[1], D == 3 ? x[2] : 0);
+    }
+    return gval<D>(P, L, bc, x[0], x[1], D == 3 ? x[2] : 0);
+}
+
+// restrict_edge (PKG/transfer.py:76-91; KER/numpy_backend.py:162-191) for
+// edge axis ea: the reference runs the axis-0 kernel on a moveaxis view
+// whose axes are (ea, remaining axes in order).  Thread per coarse interior
+// point; writes coarse value into the blocked coarse array.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_restrict_edge(const double* __restrict__ Fn, Lvl L,
+                                                       BcSpec bc, double* __restrict__ Co,
+                                                       Lvl Lc) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    // enumerate coarse interior points in natural order
+    long m[3];
+    const int ea = L.ea;
+    for (int a = 0; a < 3; ++a) m[a] = a < D ? (a == ea ? Lc.n[a] - 1 : Lc.n[a]) : 1;
+    if (t >= m[0] * m[1] * m[2]) return;
+    int I[3];
+    I[2] = 1 + (int)(t % m[2]);
+    long r = t / m[2];
+    I[1] = 1 + (int)(r % m[1]);
+    I[0] = 1 + (int)(r / m[1]);
+    if (D == 2) { I[2] = 0; I[1] = 1 + (int)(t % m[1]); I[0] = 1 + (int)(t / m[1]); }
+    // permuted axes: v0 = ea, v1, v2 = others in order
+    int pa[3];
+    pa[0] = ea;
+    {
+        int q = 1;
+        for (int a = 0; a < D; ++a)
+            if (a != ea) pa[q++] = a;
+    }
+    int fi = 2 * I[pa[0]], fj = 2 * I[pa[1]], fk = D == 3 ? 2 * I[pa[2]] : 0;
+    auto F = [&](int x, int y, int z) {
+        int g[3];
+        g[pa[0]] = x;
+        g[pa[1]] = y;
+        if (D == 3) g[pa[2]] = z;
+        else g[2] = 0;
+        return fval<D>(Fn, L, bc, g);
+    };
+    double res;
+    if (D == 2) {
+        double t1 = ad(ad(F(fi - 1, fj - 1, 0), ml(2.0, F(fi - 1, fj, 0))), F(fi - 1, fj + 1, 0));
+        double t2 = ad(ad(F(fi, fj - 1, 0), ml(2.0, F(fi, fj, 0))), F(fi, fj + 1, 0));
+        res = ml(ad(t1, t2), 0.125);
+    } else {
+        double tang[2];
+#pragma unroll
+        for (int cI = 0; cI < 2; ++cI) {
+            int fx = fi - 1 + cI;
+            double rows[3];
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr) {
+                int fy = fj - 1 + rr;
+                rows[rr] = ml(ad(ad(F(fx, fy, fk - 1), ml(2.0, F(fx, fy, fk))), F(fx, fy, fk + 1)),
+                              0.25);
+            }
+            tang[cI] = ml(ad(ad(rows[0], ml(2.0, rows[1])), rows[2]), 0.25);
+        }
+        res = ml(ad(tang[0], tang[1]), 0.5);
+    }
+    int cc = 0, cb[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        cc |= (I[a] & 1) << (D - 1 - a);
+        cb[a] = (I[a] + 1) >> 1;
+    }
+    Co[at<D>(Lc, cc, cb[0], cb[1], cb[2])] = res;
+}
+
+// PINIT = P_c (interior) for edge fields
+template <int D>
+__global__ void k_copy_blk(const double* __restrict__ src, double* __restrict__ dst, long n) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t < n) dst[t] = src[t];
+}
+
+// Correction value c = p_c - pinit at coarse grid index x, with homogenized
+// ghosts (PKG/fas.py:119-121).  The periodic low wall of p_c is never
+// written in the reference (zero for solver-owned coarse fields) and the
+// interior subtraction leaves it unchanged.
+template <int D>
+struct CorrReader {
+    const double* Pc;
+    const double* PI;
+    Lvl L;
+    __device__ double operator()(int x0, int x1, int x2) const {
+        int x[3] = {x0, x1, x2};
+        int c = 0, b[3] = {0, 0, 0};
+        bool wall = false;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            c |= (x[a] & 1) << (D - 1 - a);
+            b[a] = (x[a] + 1) >> 1;
+            if (a == L.ea && x[a] == 0) wall = true;
+        }
+        long o = at<D>(L, c, b[0], b[1], b[2]);
+        if (wall) return Pc[o];
+        return sb(Pc[o], PI[o]);
+    }
+};
+
+// prolong_edge (PKG/transfer.py:94-109; KER/numpy_backend.py:194-224) of the
+// correction, added to the fine interior (PKG/fas.py:122-123).  Thread per
+// fine interior point.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_correct_edge(double* __restrict__ P, Lvl L,
+                                                      const double* __restrict__ Pc,
+                                                      const double* __restrict__ PI, Lvl Lc,
+                                                      BcSpec bch) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+    const int ea = L.ea;
+    int pa[3];
+    pa[0] = ea;
+    {
+        int q = 1;
+        for (int a = 0; a < D; ++a)
+            if (a != ea) pa[q++] = a;
+    }
+    AxisGeo ax[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        ax[a].m = a < D ? Lc.n[a] : 1;
+        ax[a].edge = (a == ea);
+    }
+    CorrReader<D> rd{Pc, PI, Lc};
+    // coarse value at permuted coarse index (i, j, k)
+    auto C = [&](int i, int j, int k) {
+        int g[3];
+        g[pa[0]] = i;
+        g[pa[1]] = j;
+        if (D == 3) g[pa[2]] = k;
+        else g[2] = 0;
+        bool in = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            int hi = (a == ea) ? Lc.n[a] - 1 : Lc.n[a];
+            in = in && g[a] >= 1 && g[a] <= hi;
+        }
+        if (in) return rd(g[0], g[1], D == 3 ? g[2] : 0);
+        return ghost_value<D>(ax, bch, g[0], g[1], D == 3 ? g[2] : 0, rd);
+    };
+    // value of the prolonged field on coarse line i (fine column 2i) at fine
+    // tangential indices (fy, fz)
+    auto line = [&](int i, int fy, int fz) {
+        int j = (fy + 1) >> 1, dj = (fy & 1) ? -1 : 1;
+        if (D == 2) return ml(ad(ml(3.0, C(i, j, 0)), C(i, j + dj, 0)), 0.25);
+        int k = (fz + 1) >> 1, dk = (fz & 1) ? -1 : 1;
+        double t_near = ml(ad(ml(3.0, C(i, j, k)), C(i, j + dj, k)), 0.25);
+        double t_far = ml(ad(ml(3.0, C(i, j, k + dk)), C(i, j + dj, k + dk)), 0.25);
+        return ml(ad(ml(3.0, t_near), t_far), 0.25);
+    };
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (!interior<D>(L, c, bb)) continue;
+        int x[3] = {0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = 2 * bb[a] - qbit<D>(c, a);
+        int fx = x[pa[0]], fy = x[pa[1]], fz = D == 3 ? x[pa[2]] : 0;
+        double v;
+        if ((fx & 1) == 0) v = line(fx >> 1, fy, fz);
+        else v = ml(ad(line(fx >> 1, fy, fz), line((fx >> 1) + 1, fy, fz)), 0.5);
+        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+        P[o] = ad(P[o], v);
+    }
+}
+
+// ------------------------------------------------- outer residual norm
+// sum over interior points of r^2 with r = f - (a p - b Lap p); per-CTA
+// partial sums in a fixed tree order, then a single-CTA fixed-order final
+// reduction (deterministic, run-to-run stable).
+template <int D>
+__global__ void __launch_bounds__(TPB) k_res_sumsq(const double* __restrict__ P,
+                                                   const double* __restrict__ F, Lvl L,
+                                                   BcSpec bc, double* __restrict__ part) {
+    __shared__ double sh[TPB / 32];
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    double acc = 0.0;
+    if (t < L.nblk) {
+        int bb[3];
+        decode<D>(L, t, bb);
+#pragma unroll
+        for (int c = 0; c < (1 << D); ++c) {
+            if (!interior<D>(L, c, bb)) continue;
+            const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+            const double r = sb(F[o], op_at<D>(P, L, bc, c, bb, o));
+            acc = ad(acc, ml(r, r));
+        }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc = ad(acc, __shfl_down_sync(0xffffffffu, acc, s));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = sh[0];
+        for (int w = 1; w < TPB / 32; ++w) s = ad(s, sh[w]);
+        part[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_final_sum(const double* __restrict__ part, int n, double* out) {
+    __shared__ double sh[1024];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc = ad(acc, part[i]);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sh[threadIdx.x] = ad(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// ------------------------------------------------------- pack / unpack
+// natural core view (strides) <-> blocked arrays.  pack covers core
+// indices 0..M+1 (cell) / 0..n (edge axis) so stored walls travel too.
+template <int D>
+__global__ void k_pack(const double* __restrict__ src, long s0, long s1, long s2,
+                       double* __restrict__ dst, Lvl L, int e0, int e1, int e2) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    long tot = (long)e0 * e1 * (D == 3 ? e2 : 1);
+    if (t >= tot) return;
+    int x[3];
+    if (D == 3) {
+        x[2] = (int)(t % e2);
+        long r = t / e2;
+        x[1] = (int)(r % e1);
+        x[0] = (int)(r / e1);
+    } else {
+        x[1] = (int)(t % e1);
+        x[0] = (int)(t / e1);
+        x[2] = 0;
+    }
+    int c = 0, b[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c |= (x[a] & 1) << (D - 1 - a);
+        b[a] = (x[a] + 1) >> 1;
+    }
+    dst[at<D>(L, c, b[0], b[1], b[2])] = src[x[0] * s0 + x[1] * s1 + (long)x[2] * s2];
+}
+
+// interior only (core indices 1..M)
+template <int D>
+__global__ void k_unpack(const double* __restrict__ src, Lvl L, double* __restrict__ dst,
+                         long s0, long s1, long s2, int m0, int m1, int m2) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    long tot = (long)m0 * m1 * (D == 3 ? m2 : 1);
+    if (t >= tot) return;
+    int x[3];
+    if (D == 3) {
+        x[2] = 1 + (int)(t % m2);
+        long r = t / m2;
+        x[1] = 1 + (int)(r % m1);
+        x[0] = 1 + (int)(r / m1);
+    } else {
+        x[1] = 1 + (int)(t % m1);
+        x[0] = 1 + (int)(t / m1);
+        x[2] = 0;
+    }
+    int c = 0, b[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        c |= (x[a] & 1) << (D - 1 - a);
+        b[a] = (x[a] + 1) >> 1;
+    }
+    dst[x[0] * s0 + x[1] * s1 + (long)x[2] * s2] = src[at<D>(L, c, b[0], b[1], b[2])];
+}
+
+static inline int nb(long n, int t) { return (int)((n + t - 1) / t); }
+
+// ===========================================================================
+// Host engine
+// ===========================================================================
+struct Engine {
+    int dim, ea, nl, s;
+    Lvl L[32];
+    double* P[32] = {};
+    double* F[32] = {};
+    double* R[32] = {};
+    double* PI[32] = {};
+    double* part = nullptr;
+    double* dsum = nullptr;  // device scalar
+    double* hsum = nullptr;  // pinned host scalar
+    int npart = 0;
+    BcSpec bc, bch;
+    std::vector<unsigned> masks;  // per smoothing step, class masks in order
+    cudaStream_t stream = nullptr;
+    cudaGraph_t graph_v = nullptr, graph_vn = nullptr;
+    cudaGraphExec_t exec_v = nullptr, exec_vn = nullptr;
+    long kernels_per_vcycle = 0;
+};
+
+template <int D>
+static void launch_smooth(Engine& E, int k, long& cnt) {
+    const Lvl& L = E.L[k];
+    for (int it = 0; it < E.s; ++it)
+        for (unsigned m : E.masks) {
+            k_sweep<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, m);
+            ++cnt;
+        }
+}
+
+template <int D>
+static void launch_vcycle(Engine& E, long& cnt) {
+    // descent
+    for (int k = 0; k < E.nl - 1; ++k) {
+        const Lvl& L = E.L[k];
+        const Lvl& Lc = E.L[k + 1];
+        launch_smooth<D>(E, k, cnt);
+        if (E.ea < 0) {
+            k_tau_cell<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc,
+                                                                 E.P[k + 1], E.F[k + 1], Lc);
+            ++cnt;
+        } else {
+            k_residual<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], E.F[k], E.R[k], L,
+                                                                 E.bc);
+            long mc = 1;
+            for (int a = 0; a < D; ++a) mc *= (a == E.ea ? Lc.n[a] - 1 : Lc.n[a]);
+            k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.bc, E.P[k + 1],
+                                                                  Lc);
+            k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.R[k], L, E.bch, E.F[k + 1],
+                                                                  Lc);
+            long tot = Lc.cls * (1 << D);
+            k_copy_blk<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], tot);
+            cnt += 4;
+        }
+        k_coarse_src<D><<<nb(Lc.nblk, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.F[k + 1], Lc,
+                                                                E.bc);
+        ++cnt;
+    }
+    launch_smooth<D>(E, E.nl - 1, cnt);  // coarsest: s smoothing steps
+    // ascent
+    for (int k = E.nl - 2; k >= 0; --k) {
+        const Lvl& L = E.L[k];
+        const Lvl& Lc = E.L[k + 1];
+        if (E.ea < 0)
+            k_correct_cell<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc);
+        else
+            k_correct_edge<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1],
+                                                                     E.PI[k + 1], Lc, E.bch);
+        ++cnt;
+        launch_smooth<D>(E, k, cnt);
+    }
+}
+
+template <int D>
+static void launch_norm(Engine& E, long& cnt) {
+    const Lvl& L = E.L[0];
+    k_res_sumsq<D><<<E.npart, TPB, 0, E.stream>>>(E.P[0], E.F[0], L, E.bc, E.part);
+    k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, E.npart, E.dsum);
+    cnt += 2;
+}
+
+static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* ex) {
+    long cnt = 0;
+    cudaError_t e = cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return fasmg_check(e);
+    if (E.dim == 3) {
+        launch_vcycle<3>(E, cnt);
+        if (with_norm) launch_norm<3>(E, cnt);
+    } else {
+        launch_vcycle<2>(E, cnt);
+        if (with_norm) launch_norm<2>(E, cnt);
+    }
+    if (with_norm) {
+        cudaMemcpyAsync(E.hsum, E.dsum, sizeof(double), cudaMemcpyDeviceToHost, E.stream);
+    }
+    e = cudaStreamEndCapture(E.stream, g);
+    if (e != cudaSuccess) return fasmg_check(e);
+    e = cudaGraphInstantiate(ex, *g, 0);
+    if (e != cudaSuccess) return fasmg_check(e);
+    if (!with_norm) E.kernels_per_vcycle = cnt;
+    return 0;
+}
+
+static Lvl make_lvl(int dim, const int* n, int ea, double dmin, double dmax, double a,
+                    double b) {
+    Lvl L;
+    memset(&L, 0, sizeof(L));
+    L.dim = dim;
+    L.ea = ea;
+    L.nblk = 1;
+    for (int t = 0; t < 3; ++t) {
+        L.n[t] = t < dim ? n[t] : 2;
+        L.B[t] = L.n[t] / 2;
+        L.E[t] = L.B[t] + 2;
+        if (t < dim) L.nblk *= L.B[t];
+    }
+    int last = dim - 1;
+    long pitch = ((long)L.E[last] + OFF + 3) / 4 * 4;
+    if (dim == 3) {
+        L.s1 = pitch;
+        L.s0 = pitch * L.E[1];
+        L.cls = L.s0 * L.E[0];
+    } else {
+        L.s1 = 1;
+        L.s0 = pitch;
+        L.cls = pitch * L.E[0];
+    }
+    L.cls = (L.cls + 31) / 32 * 32;  // 256-byte aligned class arrays
+    // scalars exactly as the reference computes them (PKG/grid.py:71-73,
+    // PKG/smoothers.py:143-144, PKG/stencil.py:37-38,58)
+    L.h = (dmax - dmin) / n[0];
+    L.h2 = L.h * L.h;
+    L.inv_h2 = 1.0 / (L.h * L.h);
+    L.a = a;
+    L.b = b;
+    L.denom = a * L.h2 + (double)(2 * dim) * b;
+    return L;
+}
+
+}  // namespace fasmg
+
+using namespace fasmg;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+// masks: one uint32 per color group (classes updated after one ghost
+// refresh); the smoother of one smoothing step runs them in order.
+void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dmax,
+                          int mesh_level, double a, double b, const int* kinds,
+                          const double* vals, int nmasks, const unsigned* masks, int s,
+                          void* stream) {
+    if (dim != 2 && dim != 3) { fasmg_set_error(FASMG_EINVAL, "dim must be 2 or 3"); return nullptr; }
+    if (mesh_level < 1 || mesh_level > 30) { fasmg_set_error(FASMG_EINVAL, "bad mesh_level"); return nullptr; }
+    for (int t = 0; t < dim; ++t)
+        if (n[t] % (1 << mesh_level) != 0 || (n[t] >> mesh_level) % 2 != 0) {
+            fasmg_set_error(FASMG_EINVAL, "grid does not stay even through mesh_level coarsenings");
+            return nullptr;
+        }
+    Engine* E = new Engine();
+    E->dim = dim;
+    E->ea = ea;
+    E->nl = mesh_level + 1;
+    E->s = s;
+    E->stream = (cudaStream_t)stream;
+    for (int t = 0; t < 3; ++t)
+        for (int sd = 0; sd < 2; ++sd) {
+            E->bc.kind[t][sd] = t < dim ? kinds[2 * t + sd] : 0;
+            E->bc.val[t][sd] = t < dim ? vals[2 * t + sd] : 0.0;
+            E->bch.kind[t][sd] = E->bc.kind[t][sd];
+            E->bch.val[t][sd] = 0.0;  // PKG/boundary.py:83-87
+        }
+    E->masks.assign(masks, masks + nmasks);
+    int nn[3] = {n[0], n[1], dim == 3 ? n[2] : 2};
+    for (int k = 0; k < E->nl; ++k) {
+        E->L[k] = make_lvl(dim, nn, ea, dmin, dmax, a, b);
+        size_t bytes = sizeof(double) * (size_t)E->L[k].cls * (1u << dim);
+        if (fasmg_check(cudaMalloc(&E->P[k], bytes)) || fasmg_check(cudaMalloc(&E->F[k], bytes))) {
+            delete E;
+            return nullptr;
+        }
+        cudaMemsetAsync(E->P[k], 0, bytes, E->stream);
+        cudaMemsetAsync(E->F[k], 0, bytes, E->stream);
+        if (ea >= 0) {
+            if (k < E->nl - 1 && fasmg_check(cudaMalloc(&E->R[k], bytes))) { delete E; return nullptr; }
+            if (k >= 1 && fasmg_check(cudaMalloc(&E->PI[k], bytes))) { delete E; return nullptr; }
+            if (k < E->nl - 1) cudaMemsetAsync(E->R[k], 0, bytes, E->stream);
+            if (k >= 1) cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
+        }
+        for (int t = 0; t < dim; ++t) nn[t] /= 2;
+    }
+    E->npart = nb(E->L[0].nblk, TPB);
+    if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
+        fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
+        fasmg_check(cudaMallocHost(&E->hsum, sizeof(double)))) {
+        delete E;
+        return nullptr;
+    }
+    if (fasmg_check(cudaStreamSynchronize(E->stream))) { delete E; return nullptr; }
+    return E;
+}
+
+void fasmg_engine_destroy(void* h) {
+    Engine* E = (Engine*)h;
+    if (!E) return;
+    cudaStreamSynchronize(E->stream);
+    if (E->exec_v) cudaGraphExecDestroy(E->exec_v);
+    if (E->exec_vn) cudaGraphExecDestroy(E->exec_vn);
+    if (E->graph_v) cudaGraphDestroy(E->graph_v);
+    if (E->graph_vn) cudaGraphDestroy(E->graph_vn);
+    for (int k = 0; k < E->nl; ++k) {
+        cudaFree(E->P[k]);
+        cudaFree(E->F[k]);
+        if (E->R[k]) cudaFree(E->R[k]);
+        if (E->PI[k]) cudaFree(E->PI[k]);
+    }
+    cudaFree(E->part);
+    cudaFree(E->dsum);
+    cudaFreeHost(E->hsum);
+    delete E;
+}
+
+// Load p and f (natural core views) into the engine's finest level.
+int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double* fcore,
+                      const long* fs) {
+    Engine* E = (Engine*)h;
+    const Lvl& L = E->L[0];
+    int e[3];
+    for (int a = 0; a < 3; ++a) e[a] = a < E->dim ? (a == E->ea ? L.n[a] + 1 : L.n[a] + 2) : 1;
+    long tot = (long)e[0] * e[1] * e[2];
+    if (E->dim == 3) {
+        k_pack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(pcore, ps[0], ps[1], ps[2], E->P[0], L,
+                                                        e[0], e[1], e[2]);
+        k_pack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(fcore, fs[0], fs[1], fs[2], E->F[0], L,
+                                                        e[0], e[1], e[2]);
+    } else {
+        k_pack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(pcore, ps[0], ps[1], 0, E->P[0], L, e[0],
+                                                        e[1], 1);
+        k_pack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(fcore, fs[0], fs[1], 0, E->F[0], L, e[0],
+                                                        e[1], 1);
+    }
+    return fasmg_check_launch();
+}
+
+// Store the finest-level solution interior into a natural core view.
+int fasmg_engine_store(void* h, double* pcore, const long* ps) {
+    Engine* E = (Engine*)h;
+    const Lvl& L = E->L[0];
+    int m[3];
+    for (int a = 0; a < 3; ++a) m[a] = a < E->dim ? (a == E->ea ? L.n[a] - 1 : L.n[a]) : 1;
+    long tot = (long)m[0] * m[1] * m[2];
+    if (E->dim == 3)
+        k_unpack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], ps[2],
+                                                          m[0], m[1], m[2]);
+    else
+        k_unpack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], 0,
+                                                          m[0], m[1], 1);
+    return fasmg_check_launch();
+}
+
+// Enqueue `count` V-cycles; when with_norm, each is followed by the outer
+// residual norm's sum of squares, and the LAST one is copied to *sumsq
+// after synchronizing (returned through the pinned scalar).
+int fasmg_engine_run(void* h, int count, int with_norm, double* sumsq, int use_graph) {
+    Engine* E = (Engine*)h;
+    int st;
+    for (int it = 0; it < count; ++it) {
+        if (use_graph) {
+            cudaGraphExec_t* ex = with_norm ? &E->exec_vn : &E->exec_v;
+            cudaGraph_t* g = with_norm ? &E->graph_vn : &E->graph_v;
+            if (!*ex && (st = capture(*E, with_norm != 0, g, ex))) return st;
+            if ((st = fasmg_check(cudaGraphLaunch(*ex, E->stream)))) return st;
+        } else {
+            long cnt = 0;
+            if (E->dim == 3) {
+                launch_vcycle<3>(*E, cnt);
+                if (with_norm) launch_norm<3>(*E, cnt);
+            } else {
+                launch_vcycle<2>(*E, cnt);
+                if (with_norm) launch_norm<2>(*E, cnt);
+            }
+            if (with_norm)
+                cudaMemcpyAsync(E->hsum, E->dsum, sizeof(double), cudaMemcpyDeviceToHost,
+                                E->stream);
+            if ((st = fasmg_check_launch())) return st;
+        }
+    }
+    if (with_norm) {
+        if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
+        *sumsq = *E->hsum;
+    }
+    return 0;
+}
+
+// Residual sum of squares of the current finest state (no V-cycle).
+int fasmg_engine_residual_sumsq(void* h, double* sumsq) {
+    Engine* E = (Engine*)h;
+    long cnt = 0;
+    if (E->dim == 3) launch_norm<3>(*E, cnt);
+    else launch_norm<2>(*E, cnt);
+    cudaMemcpyAsync(E->hsum, E->dsum, sizeof(double), cudaMemcpyDeviceToHost, E->stream);
+    int st = fasmg_check(cudaStreamSynchronize(E->stream));
+    if (!st) *sumsq = *E->hsum;
+    return st;
+}
+
+long fasmg_engine_kernels_per_vcycle(void* h) { return ((Engine*)h)->kernels_per_vcycle; }
+
+// Device pointer and geometry of a level's blocked arrays (tests/bench).
+int fasmg_engine_level_info(void* h, int k, long* info) {
+    Engine* E = (Engine*)h;
+    if (k < 0 || k >= E->nl) return fasmg_set_error(FASMG_EINVAL, "level out of range");
+    const Lvl& L = E->L[k];
+    info[0] = L.nblk;
+    info[1] = L.cls;
+    info[2] = L.n[0];
+    info[3] = L.n[1];
+    info[4] = L.n[2];
+    return 0;
+}
+
+}  // extern "C"

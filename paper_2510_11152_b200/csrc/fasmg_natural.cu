@@ -1,0 +1,793 @@
+// fasmg_natural.cu -- the reference kernel ABI on device arrays in the
+// reference (natural) layout, plus ghost fill and numpy-ordered reductions.
+//
+// These are the drop-in replacements for the 16 names dispatched by
+// KER/__init__.py:37-46 (signatures of KER/numpy_backend.py), taking device
+// pointers to core views with element strides.  The fast FAS V-cycle does
+// not use them (it runs on the parity-blocked layout, fasmg_engine.cu); they
+// back the field-level API (smooth, residual, restrict, ... on Field
+// objects) and the WENO / staggered operators of the projection drivers.
+#include "fasmg_common.cuh"
+#include "fasmg_internal.h"
+
+namespace fasmg {
+
+#define I2(s, i, j) ((long)(i) * (s)[0] + (long)(j) * (s)[1])
+#define I3(s, i, j, k) ((long)(i) * (s)[0] + (long)(j) * (s)[1] + (long)(k) * (s)[2])
+
+struct S3 { long s[3]; };
+
+static inline S3 mk(const long* st) { S3 r; r.s[0] = st[0]; r.s[1] = st[1]; r.s[2] = st[2]; return r; }
+
+static inline int nblk(long n, int t) { return (int)((n + t - 1) / t); }
+static constexpr int TPB = 256;
+
+// ---------------------------------------------------------------- GS sweeps
+// KER/numpy_backend.py:27-62: p = (h2*f + b*nsum)/denom, nsum in E,W,N,S,T,B
+__global__ void k_gs2(double* p, S3 ps, const double* f, S3 fs, double b, double h2,
+                      double denom, int i0, int j0, int ni, int nj) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)ni * nj) return;
+    int i = i0 + 2 * (int)(t / nj), j = j0 + 2 * (int)(t % nj);
+    double nsum = ad(ad(ad(p[I2(ps.s, i + 1, j)], p[I2(ps.s, i - 1, j)]), p[I2(ps.s, i, j + 1)]),
+                     p[I2(ps.s, i, j - 1)]);
+    p[I2(ps.s, i, j)] = dv(ad(ml(h2, f[I2(fs.s, i, j)]), ml(b, nsum)), denom);
+}
+
+__global__ void k_gs3(double* p, S3 ps, const double* f, S3 fs, double b, double h2,
+                      double denom, int i0, int j0, int k0, int ni, int nj, int nk) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)ni * nj * nk) return;
+    int k = k0 + 2 * (int)(t % nk);
+    long r = t / nk;
+    int j = j0 + 2 * (int)(r % nj), i = i0 + 2 * (int)(r / nj);
+    double nsum = ad(ad(ad(ad(ad(p[I3(ps.s, i + 1, j, k)], p[I3(ps.s, i - 1, j, k)]),
+                                 p[I3(ps.s, i, j + 1, k)]), p[I3(ps.s, i, j - 1, k)]),
+                           p[I3(ps.s, i, j, k + 1)]), p[I3(ps.s, i, j, k - 1)]);
+    p[I3(ps.s, i, j, k)] = dv(ad(ml(h2, f[I3(fs.s, i, j, k)]), ml(b, nsum)), denom);
+}
+
+static inline int prng(int lo, int par) { return lo + ((par - lo) & 1); }
+
+// ----------------------------------------------------- apply_op / residual
+// KER/numpy_backend.py:69-112
+template <bool RES>
+__global__ void k_op2(double* out, S3 os, const double* p, S3 ps, const double* fsrc, S3 fs,
+                      double a, double b, double inv_h2, int ilo, int jlo, int ni, int nj) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)ni * nj) return;
+    int i = ilo + (int)(t / nj), j = jlo + (int)(t % nj);
+    double c = p[I2(ps.s, i, j)];
+    double nsum = ad(ad(ad(p[I2(ps.s, i + 1, j)], p[I2(ps.s, i - 1, j)]), p[I2(ps.s, i, j + 1)]),
+                     p[I2(ps.s, i, j - 1)]);
+    double lap = ml(sb(nsum, ml(4.0, c)), inv_h2);
+    double op = sb(ml(a, c), ml(b, lap));
+    out[I2(os.s, i, j)] = RES ? sb(fsrc[I2(fs.s, i, j)], op) : op;
+}
+
+template <bool RES>
+__global__ void k_op3(double* out, S3 os, const double* p, S3 ps, const double* fsrc, S3 fs,
+                      double a, double b, double inv_h2, int ilo, int jlo, int klo, int ni,
+                      int nj, int nk) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)ni * nj * nk) return;
+    int k = klo + (int)(t % nk);
+    long r = t / nk;
+    int j = jlo + (int)(r % nj), i = ilo + (int)(r / nj);
+    double c = p[I3(ps.s, i, j, k)];
+    double nsum = ad(ad(ad(ad(ad(p[I3(ps.s, i + 1, j, k)], p[I3(ps.s, i - 1, j, k)]),
+                                 p[I3(ps.s, i, j + 1, k)]), p[I3(ps.s, i, j - 1, k)]),
+                           p[I3(ps.s, i, j, k + 1)]), p[I3(ps.s, i, j, k - 1)]);
+    double lap = ml(sb(nsum, ml(6.0, c)), inv_h2);
+    double op = sb(ml(a, c), ml(b, lap));
+    out[I3(os.s, i, j, k)] = RES ? sb(fsrc[I3(fs.s, i, j, k)], op) : op;
+}
+
+// -------------------------------------------------- cell-centered transfers
+// KER/numpy_backend.py:119-155 (3D add order: numba :238-253)
+__global__ void k_rcc2(const double* fn, S3 fs, double* co, S3 cs, int m0, int n0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)m0 * n0) return;
+    int i = 1 + (int)(t / n0), j = 1 + (int)(t % n0);
+    int fi = 2 * i, fj = 2 * j;
+    double acc = ad(ad(ad(fn[I2(fs.s, fi - 1, fj - 1)], fn[I2(fs.s, fi - 1, fj)]),
+                       fn[I2(fs.s, fi, fj - 1)]), fn[I2(fs.s, fi, fj)]);
+    co[I2(cs.s, i, j)] = ml(acc, 0.25);
+}
+
+__global__ void k_rcc3(const double* fn, S3 fs, double* co, S3 cs, int m0, int n0, int l0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)m0 * n0 * l0) return;
+    int k = 1 + (int)(t % l0);
+    long r = t / l0;
+    int j = 1 + (int)(r % n0), i = 1 + (int)(r / n0);
+    int fi = 2 * i, fj = 2 * j, fk = 2 * k;
+    double acc = fn[I3(fs.s, fi - 1, fj - 1, fk - 1)];
+    acc = ad(acc, fn[I3(fs.s, fi - 1, fj - 1, fk)]);
+    acc = ad(acc, fn[I3(fs.s, fi - 1, fj, fk - 1)]);
+    acc = ad(acc, fn[I3(fs.s, fi - 1, fj, fk)]);
+    acc = ad(acc, fn[I3(fs.s, fi, fj - 1, fk - 1)]);
+    acc = ad(acc, fn[I3(fs.s, fi, fj - 1, fk)]);
+    acc = ad(acc, fn[I3(fs.s, fi, fj, fk - 1)]);
+    acc = ad(acc, fn[I3(fs.s, fi, fj, fk)]);
+    co[I3(cs.s, i, j, k)] = ml(acc, 0.125);
+}
+
+__global__ void k_pcc2(const double* co, S3 cs, double* fn, S3 fs, int m0, int n0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)m0 * n0) return;
+    int i = 1 + (int)(t / n0), j = 1 + (int)(t % n0);
+    int fi = 2 * i, fj = 2 * j;
+    double c = co[I2(cs.s, i, j)];
+    fn[I2(fs.s, fi - 1, fj - 1)] = c;
+    fn[I2(fs.s, fi - 1, fj)] = c;
+    fn[I2(fs.s, fi, fj - 1)] = c;
+    fn[I2(fs.s, fi, fj)] = c;
+}
+
+__global__ void k_pcc3(const double* co, S3 cs, double* fn, S3 fs, int m0, int n0, int l0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)m0 * n0 * l0) return;
+    int k = 1 + (int)(t % l0);
+    long r = t / l0;
+    int j = 1 + (int)(r % n0), i = 1 + (int)(r / n0);
+    int fi = 2 * i, fj = 2 * j, fk = 2 * k;
+    double c = co[I3(cs.s, i, j, k)];
+    for (int di = -1; di <= 0; ++di)
+        for (int dj = -1; dj <= 0; ++dj)
+            for (int dk = -1; dk <= 0; ++dk) fn[I3(fs.s, fi + di, fj + dj, fk + dk)] = c;
+}
+
+// --------------------------------------------------- edge-axis-0 transfers
+// KER/numpy_backend.py:162-224
+__global__ void k_red2(const double* fn, S3 fs, double* co, S3 cs, int m0, int n0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)(m0 - 1) * n0) return;
+    int i = 1 + (int)(t / n0), j = 1 + (int)(t % n0);
+    int fi = 2 * i, fj = 2 * j;
+    double t1 = ad(ad(fn[I2(fs.s, fi - 1, fj - 1)], ml(2.0, fn[I2(fs.s, fi - 1, fj)])),
+                   fn[I2(fs.s, fi - 1, fj + 1)]);
+    double t2 = ad(ad(fn[I2(fs.s, fi, fj - 1)], ml(2.0, fn[I2(fs.s, fi, fj)])),
+                   fn[I2(fs.s, fi, fj + 1)]);
+    co[I2(cs.s, i, j)] = ml(ad(t1, t2), 0.125);
+}
+
+__device__ __forceinline__ double red3_point(const double* fn, const S3& fs, int i, int j,
+                                             int k) {
+    int fi = 2 * i, fj = 2 * j, fk = 2 * k;
+    double tang[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        int fx = fi - 1 + c;
+        double rows[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            int fy = fj - 1 + r;
+            rows[r] = ml(ad(ad(fn[I3(fs.s, fx, fy, fk - 1)], ml(2.0, fn[I3(fs.s, fx, fy, fk)])),
+                            fn[I3(fs.s, fx, fy, fk + 1)]), 0.25);
+        }
+        tang[c] = ml(ad(ad(rows[0], ml(2.0, rows[1])), rows[2]), 0.25);
+    }
+    return ml(ad(tang[0], tang[1]), 0.5);
+}
+
+__global__ void k_red3(const double* fn, S3 fs, double* co, S3 cs, int m0, int n0, int l0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)(m0 - 1) * n0 * l0) return;
+    int k = 1 + (int)(t % l0);
+    long r = t / l0;
+    int j = 1 + (int)(r % n0), i = 1 + (int)(r / n0);
+    co[I3(cs.s, i, j, k)] = red3_point(fn, fs, i, j, k);
+}
+
+__global__ void k_ped2_lines(const double* co, S3 cs, double* fn, S3 fs, int m0, int n0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)(m0 + 1) * n0) return;
+    int i = (int)(t / n0), j = 1 + (int)(t % n0);
+    int fi = 2 * i, fj = 2 * j;
+    double cc = co[I2(cs.s, i, j)];
+    fn[I2(fs.s, fi, fj - 1)] = ml(ad(ml(3.0, cc), co[I2(cs.s, i, j - 1)]), 0.25);
+    fn[I2(fs.s, fi, fj)] = ml(ad(ml(3.0, cc), co[I2(cs.s, i, j + 1)]), 0.25);
+}
+
+__global__ void k_ped2_mid(double* fn, S3 fs, int m0, int n0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    long nn = 2L * n0;
+    if (t >= (long)m0 * nn) return;
+    int i = (int)(t / nn), fj = 1 + (int)(t % nn);
+    int fi = 2 * i + 1;
+    fn[I2(fs.s, fi, fj)] = ml(ad(fn[I2(fs.s, fi - 1, fj)], fn[I2(fs.s, fi + 1, fj)]), 0.5);
+}
+
+__global__ void k_ped3_lines(const double* co, S3 cs, double* fn, S3 fs, int m0, int n0,
+                             int l0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)(m0 + 1) * n0 * l0) return;
+    int k = 1 + (int)(t % l0);
+    long r = t / l0;
+    int j = 1 + (int)(r % n0), i = (int)(r / n0);
+    int fi = 2 * i, fj = 2 * j, fk = 2 * k;
+#pragma unroll
+    for (int dj = -1; dj <= 1; dj += 2) {
+        double t_near = ml(ad(ml(3.0, co[I3(cs.s, i, j, k)]), co[I3(cs.s, i, j + dj, k)]), 0.25);
+#pragma unroll
+        for (int dk = -1; dk <= 1; dk += 2) {
+            double t_far = ml(ad(ml(3.0, co[I3(cs.s, i, j, k + dk)]),
+                                 co[I3(cs.s, i, j + dj, k + dk)]), 0.25);
+            int fy = dj == -1 ? fj - 1 : fj;
+            int fz = dk == -1 ? fk - 1 : fk;
+            fn[I3(fs.s, fi, fy, fz)] = ml(ad(ml(3.0, t_near), t_far), 0.25);
+        }
+    }
+}
+
+__global__ void k_ped3_mid(double* fn, S3 fs, int m0, int n0, int l0) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    long nj = 2L * n0, nk = 2L * l0;
+    if (t >= (long)m0 * nj * nk) return;
+    int fk = 1 + (int)(t % nk);
+    long r = t / nk;
+    int fj = 1 + (int)(r % nj), i = (int)(r / nj);
+    int fi = 2 * i + 1;
+    fn[I3(fs.s, fi, fj, fk)] =
+        ml(ad(fn[I3(fs.s, fi - 1, fj, fk)], fn[I3(fs.s, fi + 1, fj, fk)]), 0.5);
+}
+
+// ------------------------------------------------------------------ WENO3
+// KER/numpy_backend.py:231-277 / numba :394-410
+__device__ __forceinline__ double weno_point(double dm2, double dm1, double dp1, double dp2,
+                                             double w, double inv_2h, double eps) {
+    double c0, c1, r0, r1;
+    if (w >= 0.0) {
+        c0 = sb(ml(3.0, dm1), dm2);
+        c1 = ad(dm1, dp1);
+        r0 = sb(dm1, dm2);
+        r1 = sb(dp1, dm1);
+    } else {
+        c0 = sb(ml(3.0, dp1), dp2);
+        c1 = ad(dp1, dm1);
+        r0 = sb(dp1, dp2);
+        r1 = sb(dm1, dp1);
+    }
+    double e0 = ad(eps, ml(r0, r0));
+    double e1 = ad(eps, ml(r1, r1));
+    double a0 = dv(1.0 / 3.0, ml(e0, e0));
+    double a1 = dv(2.0 / 3.0, ml(e1, e1));
+    return ml(dv(ad(ml(a0, c0), ml(a1, c1)), ad(a0, a1)), inv_2h);
+}
+
+__global__ void k_weno2(double* out, S3 os, const double* q, S3 qs, const double* wind, S3 ws,
+                        int ni, int nj, int oi, int oj, double inv_2h, double eps) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)ni * nj) return;
+    int ii = (int)(t / nj), jj = (int)(t % nj);
+    int i = ii + oi, j = jj + oj;
+    double dm2 = sb(q[I2(qs.s, i - 1, j)], q[I2(qs.s, i - 2, j)]);
+    double dm1 = sb(q[I2(qs.s, i, j)], q[I2(qs.s, i - 1, j)]);
+    double dp1 = sb(q[I2(qs.s, i + 1, j)], q[I2(qs.s, i, j)]);
+    double dp2 = sb(q[I2(qs.s, i + 2, j)], q[I2(qs.s, i + 1, j)]);
+    double w = wind[I2(ws.s, ii, jj)];
+    long o = I2(os.s, ii, jj);
+    out[o] = ad(out[o], ml(w, weno_point(dm2, dm1, dp1, dp2, w, inv_2h, eps)));
+}
+
+__global__ void k_weno3(double* out, S3 os, const double* q, S3 qs, const double* wind, S3 ws,
+                        int ni, int nj, int nk, int oi, int oj, int ok, double inv_2h,
+                        double eps) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (long)ni * nj * nk) return;
+    int kk = (int)(t % nk);
+    long r = t / nk;
+    int jj = (int)(r % nj), ii = (int)(r / nj);
+    int i = ii + oi, j = jj + oj, k = kk + ok;
+    double dm2 = sb(q[I3(qs.s, i - 1, j, k)], q[I3(qs.s, i - 2, j, k)]);
+    double dm1 = sb(q[I3(qs.s, i, j, k)], q[I3(qs.s, i - 1, j, k)]);
+    double dp1 = sb(q[I3(qs.s, i + 1, j, k)], q[I3(qs.s, i, j, k)]);
+    double dp2 = sb(q[I3(qs.s, i + 2, j, k)], q[I3(qs.s, i + 1, j, k)]);
+    double w = wind[I3(ws.s, ii, jj, kk)];
+    long o = I3(os.s, ii, jj, kk);
+    out[o] = ad(out[o], ml(w, weno_point(dm2, dm1, dp1, dp2, w, inv_2h, eps)));
+}
+
+// --------------------------------------------------------------- ghost fill
+// PKG/boundary.py:90-156, evaluated point-wise through ghost_value().
+struct FillGeo {
+    int dim, halo;
+    AxisGeo ax[3];
+    int ext[3];     // data extents
+    long st[3];     // data strides
+    long slab_n[3]; // points per slab
+    int lo[3][3];   // per slab a, per axis b: first data index
+    int cnt[3][3];  // per slab a, per axis b: count
+};
+
+struct DataReader {
+    const double* core;
+    long st[3];
+    __device__ double operator()(int x0, int x1, int x2) const {
+        return core[(long)x0 * st[0] + (long)x1 * st[1] + (long)x2 * st[2]];
+    }
+};
+
+template <int DIM>
+__global__ void k_fill(double* data, FillGeo g, BcSpec bc) {
+    int a = blockIdx.y;
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (a >= DIM || t >= g.slab_n[a]) return;
+    int d[3] = {0, 0, 0};
+    long r = t;
+    for (int b = DIM - 1; b >= 0; --b) {
+        int c = g.cnt[a][b];
+        d[b] = g.lo[a][b] + (int)(r % c);
+        r /= c;
+    }
+    // slab a enumerates the two owned ranges of axis a: cnt counts both
+    // sides; map the linear index to the lo or hi side
+    {
+        int c_lo = g.halo;  // owned lo indices along a (data 0..halo-1 or 0..halo-2)
+        const AxisGeo& A = g.ax[a];
+        int owned_lo = A.edge ? (bc.kind[a][0] == BC_PERIODIC ? g.halo - 1 : g.halo) : g.halo;
+        (void)c_lo;
+        int q = d[a] - g.lo[a][a];
+        int dat;
+        if (q < owned_lo) dat = q;  // data indices 0..owned_lo-1
+        else {
+            int first_hi = A.edge ? (g.halo - 1 + A.m) : (g.halo + A.m);
+            dat = first_hi + (q - owned_lo);
+        }
+        d[a] = dat;
+    }
+    // core index = data index - (halo - 1)
+    int x[3] = {0, 0, 0};
+    for (int b = 0; b < DIM; ++b) x[b] = d[b] - (g.halo - 1);
+    DataReader rd;
+    rd.core = data + (long)(g.halo - 1) * (g.st[0] + g.st[1] + (DIM == 3 ? g.st[2] : 0));
+    rd.st[0] = g.st[0];
+    rd.st[1] = g.st[1];
+    rd.st[2] = DIM == 3 ? g.st[2] : 0;
+    double v = ghost_value<DIM>(g.ax, bc, x[0], x[1], DIM == 3 ? x[2] : 0, rd);
+    long off = 0;
+    for (int b = 0; b < DIM; ++b) off += (long)d[b] * g.st[b];
+    data[off] = v;
+}
+
+// ------------------------------------------------ numpy-ordered reductions
+// numpy pairwise_sum (PW_BLOCKSIZE 128); see oracle/fasmg_oracle.c.
+__device__ double pw_leaf(const double* a, long n) {
+    if (n < 8) {
+        double res = 0.;
+        for (long i = 0; i < n; ++i) res = ad(res, a[i]);
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    long i;
+    for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = ad(r[j], a[i + j]);
+    double res = ad(ad(ad(r[0], r[1]), ad(r[2], r[3])), ad(ad(r[4], r[5]), ad(r[6], r[7])));
+    for (; i < n; ++i) res = ad(res, a[i]);
+    return res;
+}
+
+// iterative pairwise recursion over a contiguous buffer (post-order walk of
+// numpy's split tree: n2 = n/2 rounded down to a multiple of 8)
+__device__ double pw_sum(const double* a, long n) {
+    struct Fr { long off, len; int stage; double left; };
+    Fr stk[24];
+    int sp = 0;
+    stk[0].off = 0; stk[0].len = n; stk[0].stage = 0; stk[0].left = 0.0;
+    double ret = 0.0;
+    while (true) {
+        Fr& f = stk[sp];
+        if (f.len <= 128) {
+            ret = pw_leaf(a + f.off, f.len);
+            if (sp == 0) return ret;
+            --sp;
+            continue;
+        }
+        long n2 = f.len / 2;
+        n2 -= n2 % 8;
+        if (f.stage == 0) {
+            f.stage = 1;
+            ++sp;
+            stk[sp].off = f.off; stk[sp].len = n2; stk[sp].stage = 0;
+            continue;
+        }
+        if (f.stage == 1) {
+            f.left = ret;
+            f.stage = 2;
+            ++sp;
+            stk[sp].off = f.off + n2; stk[sp].len = f.len - n2; stk[sp].stage = 0;
+            continue;
+        }
+        ret = ad(f.left, ret);
+        if (sp == 0) return ret;
+        --sp;
+    }
+}
+
+// Per-chunk gather + pairwise sum of a C-order interior view (numpy buffered
+// reduce chunking, oracle or_reduce_chunk).  One thread per chunk; the
+// chunk is gathered into a per-thread slice of a scratch buffer.
+__global__ void k_chunk_sums(const double* v, S3 vs, int dim, int e0, int e1, int e2,
+                             long n, long B, double* scratch, double* sums, long nchunks) {
+    long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    long start = c * B;
+    long len = n - start < B ? n - start : B;
+    double* buf = scratch + start;
+    for (long t = 0; t < len; ++t) {
+        long q = start + t;
+        long off;
+        if (dim == 2) {
+            off = (q / e1) * vs.s[0] + (q % e1) * vs.s[1];
+        } else {
+            long k = q % e2, r = q / e2;
+            off = (r / e1) * vs.s[0] + (r % e1) * vs.s[1] + k * vs.s[2];
+        }
+        buf[t] = v[off];
+    }
+    sums[c] = pw_sum(buf, len);
+}
+
+__global__ void k_chunk_total(const double* sums, long nchunks, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double acc = 0.0;
+    for (long c = 0; c < nchunks; ++c) acc = ad(acc, sums[c]);
+    out[0] = acc;
+}
+
+// interior -= scalar (device scalar: out[0] / count)
+__global__ void k_sub_mean(double* v, S3 vs, int dim, int e0, int e1, int e2,
+                           const double* total, double count) {
+    long n = (long)e0 * e1 * (dim == 3 ? e2 : 1);
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double m = dv(total[0], count);
+    long off;
+    if (dim == 2) off = (t / e1) * vs.s[0] + (t % e1) * vs.s[1];
+    else {
+        long k = t % e2, r = t / e2;
+        off = (r / e1) * vs.s[0] + (r % e1) * vs.s[1] + k * vs.s[2];
+    }
+    v[off] = sb(v[off], m);
+}
+
+
+// ------------------------------------------------------ staggered operators
+// gradient_axis (PKG/stencil.py:114-125): out (contiguous, edge-interior
+// shape) = (p[x + e_axis] - p[x]) * inv_h
+__global__ void k_grad(const double* p, S3 ps, double* out, int dim, int axis, int m0, int m1,
+                       int m2, double inv_h) {
+    long n = (long)m0 * m1 * (dim == 3 ? m2 : 1);
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int x[3];
+    if (dim == 3) {
+        x[2] = 1 + (int)(t % m2);
+        long r = t / m2;
+        x[1] = 1 + (int)(r % m1);
+        x[0] = 1 + (int)(r / m1);
+    } else {
+        x[1] = 1 + (int)(t % m1);
+        x[0] = 1 + (int)(t / m1);
+        x[2] = 0;
+    }
+    long lo = I3(ps.s, x[0], x[1], x[2]);
+    long hi = lo + ps.s[axis];
+    out[t] = ml(sb(p[hi], p[lo]), inv_h);
+}
+
+// divergence_edges_to_cc (PKG/stencil.py:128-156): out interior view =
+// sum_axis (c_a[x] - c_a[x - e_a]) * inv_h, accumulated in axis order.
+struct Comps { const double* c[3]; S3 s[3]; };
+__global__ void k_div(Comps C, double* out, S3 os, int dim, int n0, int n1, int n2,
+                      double inv_h) {
+    long n = (long)n0 * n1 * (dim == 3 ? n2 : 1);
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int x[3];
+    if (dim == 3) {
+        x[2] = 1 + (int)(t % n2);
+        long r = t / n2;
+        x[1] = 1 + (int)(r % n1);
+        x[0] = 1 + (int)(r / n1);
+    } else {
+        x[1] = 1 + (int)(t % n1);
+        x[0] = 1 + (int)(t / n1);
+        x[2] = 0;
+    }
+    double acc = 0.0;
+    for (int a = 0; a < dim; ++a) {
+        long hi = I3(C.s[a].s, x[0], x[1], x[2]);
+        long lo = hi - C.s[a].s[a];
+        double term = ml(sb(C.c[a][hi], C.c[a][lo]), inv_h);
+        acc = a == 0 ? term : ad(acc, term);
+    }
+    out[I3(os.s, x[0] - 1, x[1] - 1, x[2] - (dim == 3 ? 1 : 0))] = acc;
+}
+
+}  // namespace fasmg
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace fasmg;
+
+static cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+#define LAUNCH(n, ...)                                                     \
+    do {                                                                   \
+        if ((n) > 0) __VA_ARGS__;                                          \
+        return fasmg_check_launch();                                       \
+    } while (0)
+
+extern "C" {
+
+int fasmg_gs_sweep_2d(double* p, const long* ps, const double* f, const long* fs, double b,
+                      double h2, double denom, int ilo, int ihi, int jlo, int jhi, int ipar,
+                      int jpar, void* stream) {
+    int i0 = prng(ilo, ipar), j0 = prng(jlo, jpar);
+    if (i0 > ihi || j0 > jhi) return 0;
+    int ni = (ihi - i0) / 2 + 1, nj = (jhi - j0) / 2 + 1;
+    long n = (long)ni * nj;
+    LAUNCH(n, (k_gs2<<<nblk(n, TPB), TPB, 0, S(stream)>>>(p, mk(ps), f, mk(fs), b, h2, denom,
+                                                          i0, j0, ni, nj)));
+}
+
+int fasmg_gs_sweep_3d(double* p, const long* ps, const double* f, const long* fs, double b,
+                      double h2, double denom, int ilo, int ihi, int jlo, int jhi, int klo,
+                      int khi, int ipar, int jpar, int kpar, void* stream) {
+    int i0 = prng(ilo, ipar), j0 = prng(jlo, jpar), k0 = prng(klo, kpar);
+    if (i0 > ihi || j0 > jhi || k0 > khi) return 0;
+    int ni = (ihi - i0) / 2 + 1, nj = (jhi - j0) / 2 + 1, nk = (khi - k0) / 2 + 1;
+    long n = (long)ni * nj * nk;
+    LAUNCH(n, (k_gs3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(p, mk(ps), f, mk(fs), b, h2, denom,
+                                                          i0, j0, k0, ni, nj, nk)));
+}
+
+int fasmg_apply_op_2d(double* out, const long* os, const double* p, const long* ps, double a,
+                      double b, double inv_h2, int ilo, int ihi, int jlo, int jhi,
+                      void* stream) {
+    int ni = ihi - ilo + 1, nj = jhi - jlo + 1;
+    if (ni <= 0 || nj <= 0) return 0;
+    long n = (long)ni * nj;
+    LAUNCH(n, (k_op2<false><<<nblk(n, TPB), TPB, 0, S(stream)>>>(
+                  out, mk(os), p, mk(ps), nullptr, mk(ps), a, b, inv_h2, ilo, jlo, ni, nj)));
+}
+
+int fasmg_apply_op_3d(double* out, const long* os, const double* p, const long* ps, double a,
+                      double b, double inv_h2, int ilo, int ihi, int jlo, int jhi, int klo,
+                      int khi, void* stream) {
+    int ni = ihi - ilo + 1, nj = jhi - jlo + 1, nk = khi - klo + 1;
+    if (ni <= 0 || nj <= 0 || nk <= 0) return 0;
+    long n = (long)ni * nj * nk;
+    LAUNCH(n, (k_op3<false><<<nblk(n, TPB), TPB, 0, S(stream)>>>(
+                  out, mk(os), p, mk(ps), nullptr, mk(ps), a, b, inv_h2, ilo, jlo, klo, ni,
+                  nj, nk)));
+}
+
+int fasmg_residual_2d(double* out, const long* os, const double* p, const long* ps,
+                      const double* fsrc, const long* fs, double a, double b, double inv_h2,
+                      int ilo, int ihi, int jlo, int jhi, void* stream) {
+    int ni = ihi - ilo + 1, nj = jhi - jlo + 1;
+    if (ni <= 0 || nj <= 0) return 0;
+    long n = (long)ni * nj;
+    LAUNCH(n, (k_op2<true><<<nblk(n, TPB), TPB, 0, S(stream)>>>(
+                  out, mk(os), p, mk(ps), fsrc, mk(fs), a, b, inv_h2, ilo, jlo, ni, nj)));
+}
+
+int fasmg_residual_3d(double* out, const long* os, const double* p, const long* ps,
+                      const double* fsrc, const long* fs, double a, double b, double inv_h2,
+                      int ilo, int ihi, int jlo, int jhi, int klo, int khi, void* stream) {
+    int ni = ihi - ilo + 1, nj = jhi - jlo + 1, nk = khi - klo + 1;
+    if (ni <= 0 || nj <= 0 || nk <= 0) return 0;
+    long n = (long)ni * nj * nk;
+    LAUNCH(n, (k_op3<true><<<nblk(n, TPB), TPB, 0, S(stream)>>>(
+                  out, mk(os), p, mk(ps), fsrc, mk(fs), a, b, inv_h2, ilo, jlo, klo, ni, nj,
+                  nk)));
+}
+
+int fasmg_restrict_cc_2d(const double* fine, const long* fs, double* coarse, const long* cs,
+                         int m0, int n0, void* stream) {
+    long n = (long)m0 * n0;
+    LAUNCH(n, (k_rcc2<<<nblk(n, TPB), TPB, 0, S(stream)>>>(fine, mk(fs), coarse, mk(cs), m0,
+                                                           n0)));
+}
+
+int fasmg_restrict_cc_3d(const double* fine, const long* fs, double* coarse, const long* cs,
+                         int m0, int n0, int l0, void* stream) {
+    long n = (long)m0 * n0 * l0;
+    LAUNCH(n, (k_rcc3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(fine, mk(fs), coarse, mk(cs), m0,
+                                                           n0, l0)));
+}
+
+int fasmg_prolong_cc_2d(const double* coarse, const long* cs, double* fine, const long* fs,
+                        int m0, int n0, void* stream) {
+    long n = (long)m0 * n0;
+    LAUNCH(n, (k_pcc2<<<nblk(n, TPB), TPB, 0, S(stream)>>>(coarse, mk(cs), fine, mk(fs), m0,
+                                                           n0)));
+}
+
+int fasmg_prolong_cc_3d(const double* coarse, const long* cs, double* fine, const long* fs,
+                        int m0, int n0, int l0, void* stream) {
+    long n = (long)m0 * n0 * l0;
+    LAUNCH(n, (k_pcc3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(coarse, mk(cs), fine, mk(fs), m0,
+                                                           n0, l0)));
+}
+
+int fasmg_restrict_edge0_2d(const double* fine, const long* fs, double* coarse,
+                            const long* cs, int m0, int n0, void* stream) {
+    long n = (long)(m0 - 1) * n0;
+    LAUNCH(n, (k_red2<<<nblk(n, TPB), TPB, 0, S(stream)>>>(fine, mk(fs), coarse, mk(cs), m0,
+                                                           n0)));
+}
+
+int fasmg_restrict_edge0_3d(const double* fine, const long* fs, double* coarse,
+                            const long* cs, int m0, int n0, int l0, void* stream) {
+    long n = (long)(m0 - 1) * n0 * l0;
+    LAUNCH(n, (k_red3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(fine, mk(fs), coarse, mk(cs), m0,
+                                                           n0, l0)));
+}
+
+int fasmg_prolong_edge0_2d(const double* coarse, const long* cs, double* fine,
+                           const long* fs, int m0, int n0, void* stream) {
+    long n1 = (long)(m0 + 1) * n0, n2 = (long)m0 * 2 * n0;
+    if (n1 > 0)
+        k_ped2_lines<<<nblk(n1, TPB), TPB, 0, S(stream)>>>(coarse, mk(cs), fine, mk(fs), m0,
+                                                           n0);
+    if (n2 > 0) k_ped2_mid<<<nblk(n2, TPB), TPB, 0, S(stream)>>>(fine, mk(fs), m0, n0);
+    return fasmg_check_launch();
+}
+
+int fasmg_prolong_edge0_3d(const double* coarse, const long* cs, double* fine,
+                           const long* fs, int m0, int n0, int l0, void* stream) {
+    long n1 = (long)(m0 + 1) * n0 * l0, n2 = (long)m0 * 4 * n0 * l0;
+    if (n1 > 0)
+        k_ped3_lines<<<nblk(n1, TPB), TPB, 0, S(stream)>>>(coarse, mk(cs), fine, mk(fs), m0,
+                                                           n0, l0);
+    if (n2 > 0) k_ped3_mid<<<nblk(n2, TPB), TPB, 0, S(stream)>>>(fine, mk(fs), m0, n0, l0);
+    return fasmg_check_launch();
+}
+
+int fasmg_weno_deriv0_2d(double* out, const long* os, const double* q, const long* qs,
+                         const double* wind, const long* ws, int ni, int nj, int oi, int oj,
+                         double inv_2h, double eps, void* stream) {
+    long n = (long)ni * nj;
+    LAUNCH(n, (k_weno2<<<nblk(n, TPB), TPB, 0, S(stream)>>>(out, mk(os), q, mk(qs), wind,
+                                                            mk(ws), ni, nj, oi, oj, inv_2h,
+                                                            eps)));
+}
+
+int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const long* qs,
+                         const double* wind, const long* ws, int ni, int nj, int nk, int oi,
+                         int oj, int ok, double inv_2h, double eps, void* stream) {
+    long n = (long)ni * nj * nk;
+    LAUNCH(n, (k_weno3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(out, mk(os), q, mk(qs), wind,
+                                                            mk(ws), ni, nj, nk, oi, oj, ok,
+                                                            inv_2h, eps)));
+}
+
+// fill_ghosts on a natural-layout C-contiguous data array (PKG/boundary.py:90)
+int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, const int* kinds,
+                      const double* vals, void* stream) {
+    if (dim != 2 && dim != 3) return fasmg_set_error(FASMG_EINVAL, "dim must be 2 or 3");
+    FillGeo g;
+    BcSpec bc;
+    g.dim = dim;
+    g.halo = halo;
+    for (int a = 0; a < 3; ++a) {
+        for (int s = 0; s < 2; ++s) {
+            bc.kind[a][s] = a < dim ? kinds[2 * a + s] : 0;
+            bc.val[a][s] = a < dim ? vals[2 * a + s] : 0.0;
+        }
+        g.ax[a].m = a < dim ? n[a] : 1;
+        g.ax[a].edge = (a == ea);
+        g.ext[a] = a < dim ? (a == ea ? n[a] + 1 + 2 * (halo - 1) : n[a] + 2 * halo) : 1;
+    }
+    if (dim == 2) { g.st[1] = 1; g.st[0] = g.ext[1]; g.st[2] = 0; }
+    else { g.st[2] = 1; g.st[1] = g.ext[2]; g.st[0] = (long)g.ext[1] * g.ext[2]; }
+    // slab a: owned along a; not owned along axes b < a; any along b > a.
+    long maxn = 0;
+    for (int a = 0; a < dim; ++a) {
+        long cnt = 1;
+        for (int b = 0; b < dim; ++b) {
+            int c, lo;
+            const AxisGeo& B = g.ax[b];
+            int owned_lo = B.edge ? (bc.kind[b][0] == BC_PERIODIC ? halo - 1 : halo) : halo;
+            int owned_hi = B.edge ? halo : halo;  // edge: wall m + rings; cell: halo rings
+            if (b == a) { lo = 0; c = owned_lo + owned_hi; }
+            else if (b < a) { lo = owned_lo; c = g.ext[b] - owned_lo - owned_hi; }
+            else { lo = 0; c = g.ext[b]; }
+            g.lo[a][b] = lo;
+            g.cnt[a][b] = c;
+            cnt *= c;
+        }
+        g.slab_n[a] = cnt;
+        if (cnt > maxn) maxn = cnt;
+    }
+    if (maxn == 0) return 0;
+    dim3 grid(nblk(maxn, TPB), dim);
+    if (dim == 2) k_fill<2><<<grid, TPB, 0, S(stream)>>>(data, g, bc);
+    else k_fill<3><<<grid, TPB, 0, S(stream)>>>(data, g, bc);
+    return fasmg_check_launch();
+}
+
+// np.sum of an interior view in numpy's buffered-reduce order; result into
+// out[0] (device).  scratch: >= n doubles; sums: >= ceil(n/B) doubles.
+int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, double* scratch,
+                   double* sums, double* out, void* stream) {
+    long n = 1;
+    for (int a = 0; a < dim; ++a) n *= ext[a];
+    long B = 8192;
+    for (int k = 0; k < dim; ++k) {
+        long P = 1;
+        for (int a = k; a < dim; ++a) P *= ext[a];
+        if (P <= 8192) { B = (8192 / P) * P; break; }
+    }
+    long nch = (n + B - 1) / B;
+    S3 s = mk(vs);
+    if (dim == 2) s.s[2] = 0;
+    if (nch > 0)
+        k_chunk_sums<<<nblk(nch, 64), 64, 0, S(stream)>>>(v, s, dim, ext[0], ext[1],
+                                                          dim == 3 ? ext[2] : 1, n, B, scratch,
+                                                          sums, nch);
+    k_chunk_total<<<1, 32, 0, S(stream)>>>(sums, nch, out);
+    return fasmg_check_launch();
+}
+
+long fasmg_view_sum_chunks(int dim, const int* ext) {
+    long n = 1;
+    for (int a = 0; a < dim; ++a) n *= ext[a];
+    long B = 8192;
+    for (int k = 0; k < dim; ++k) {
+        long P = 1;
+        for (int a = k; a < dim; ++a) P *= ext[a];
+        if (P <= 8192) { B = (8192 / P) * P; break; }
+    }
+    return (n + B - 1) / B;
+}
+
+// v -= total[0] / count over an interior view (PKG/fas.py:145,156)
+int fasmg_sub_mean(double* v, const long* vs, int dim, const int* ext, const double* total,
+                   double count, void* stream) {
+    long n = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
+    S3 s = mk(vs);
+    if (dim == 2) s.s[2] = 0;
+    LAUNCH(n, (k_sub_mean<<<nblk(n, TPB), TPB, 0, S(stream)>>>(v, s, dim, ext[0], ext[1],
+                                                               dim == 3 ? ext[2] : 1, total,
+                                                               count)));
+}
+
+// gradient_axis: p core view; out contiguous interior of the axis' edge field
+int fasmg_gradient_axis(const double* pcore, const long* ps, double* out, int dim,
+                        const int* n, int axis, double inv_h, void* stream) {
+    int m[3];
+    for (int a = 0; a < 3; ++a) m[a] = a < dim ? (a == axis ? n[a] - 1 : n[a]) : 1;
+    long tot = (long)m[0] * m[1] * m[2];
+    S3 s = mk(ps);
+    if (dim == 2) s.s[2] = 0;
+    LAUNCH(tot, (k_grad<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(pcore, s, out, dim, axis, m[0],
+                                                               m[1], m[2], inv_h)));
+}
+
+// divergence: component core views c[a] (strides cs[3a..3a+2]); out is the
+// cell interior view (strides os)
+int fasmg_divergence(const double* const* comps, const long* cs, double* out, const long* os,
+                     int dim, const int* n, double inv_h, void* stream) {
+    Comps C;
+    for (int a = 0; a < 3; ++a) {
+        C.c[a] = a < dim ? comps[a] : nullptr;
+        for (int b = 0; b < 3; ++b) C.s[a].s[b] = a < dim ? cs[3 * a + b] : 0;
+        if (dim == 2) C.s[a].s[2] = 0;
+    }
+    S3 o = mk(os);
+    if (dim == 2) o.s[2] = 0;
+    long tot = (long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
+    LAUNCH(tot, (k_div<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(C, out, o, dim, n[0], n[1],
+                                                              dim == 3 ? n[2] : 1, inv_h)));
+}
+
+}  // extern "C"

@@ -1,0 +1,207 @@
+"""Full Approximation Storage multigrid: V-cycle and outer solve loop.
+
+Same API and semantics as PKG/fas.py (Algorithm 1):
+``FasSolver(hierarchy, location, bc, plan, coeffs)``, ``.vcycle(p, f, s)``,
+``.solve(p, f, params) -> SolveReport``, and the ``solve``/``vcycle``
+convenience wrappers.
+
+Execution: a native engine (csrc/fasmg_engine.cu, one per smoothing count
+``s``) holds every level in the parity-blocked layout, runs the V-cycle as
+one CUDA graph (smoothing half-sweeps, fused residual+restriction+tau,
+coarse source, fused prolongation+correction) and the outer residual norm,
+and returns one scalar per cycle for the ``tol`` test.  ``p`` and ``f`` are
+packed on entry and ``p`` unpacked on exit; the caller-visible state after
+``solve`` (interior, ghosts, the singular-case mean shifts of ``f`` and
+``p``) matches the reference bitwise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from .boundary import BoundaryCondition, fill_ghosts
+from .errors import NativeError
+from .grid import Field, GridHierarchy, Location, make_hierarchy, subtract_interior_mean
+from .smoothers import SweepPlan
+from .stencil import OperatorCoeffs
+
+
+@dataclass(frozen=True)
+class FasParams:
+    """tol, cycle cap, smoothing steps per stage, recursion depth
+    (PKG/fas.py:37-49)."""
+
+    tol: float
+    k_max: int
+    s: int
+    mesh_level: int
+
+    def __post_init__(self):
+        if self.tol <= 0 or self.k_max < 1 or self.s < 1 or self.mesh_level < 1:
+            raise ValueError(f"invalid solver parameters {self}")
+
+
+@dataclass
+class SolveReport:
+    iterations: int
+    residual_history: list
+    converged: bool
+
+    @property
+    def final_residual(self) -> float:
+        return self.residual_history[-1] if self.residual_history else float("nan")
+
+
+class _Engine:
+    """Owner of one native engine handle."""
+
+    def __init__(self, solver: "FasSolver", s: int, device: torch.device):
+        g = solver.hierarchy.fine
+        kinds, vals = solver.bc.codes()
+        masks = solver.plan.class_masks()
+        ea = solver.location.edge_axis
+        self.device = device
+        self.stream = N.engine_stream(device.index)
+        with torch.cuda.device(device):
+            h = N.lib().fasmg_engine_create(
+                g.dim, N.ints(g.shape), -1 if ea is None else ea,
+                float(g.domain_min[0]), float(g.domain_max[0]),
+                solver.hierarchy.mesh_level, float(solver.coeffs.a), float(solver.coeffs.b),
+                N.ints(kinds), N.doubles(vals), len(masks),
+                (ctypes.c_uint * len(masks))(*masks), int(s), self.stream)
+        if not h:
+            raise NativeError("fasmg_engine_create failed: "
+                              + N.lib().fasmg_last_error().decode(errors="replace"))
+        self.handle = ctypes.c_void_p(h)
+
+    def close(self):
+        if self.handle is not None and N._lib is not None:
+            N.lib().fasmg_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, p: Field, f: Field):
+        N.wait(self.stream, N.torch_stream())
+        pc, fc = p.core, f.core
+        N.call("fasmg_engine_load", self.handle, N.ptr(pc), N.strides(pc), N.ptr(fc),
+               N.strides(fc))
+
+    def store(self, p: Field):
+        pc = p.core
+        N.call("fasmg_engine_store", self.handle, N.ptr(pc), N.strides(pc))
+        N.wait(N.torch_stream(), self.stream)
+
+    def run(self, count: int, with_norm: bool, use_graph: bool = True) -> float:
+        out = ctypes.c_double(0.0)
+        N.call("fasmg_engine_run", self.handle, int(count), 1 if with_norm else 0,
+               ctypes.byref(out), 1 if use_graph else 0)
+        return out.value
+
+    def kernels_per_vcycle(self) -> int:
+        return int(N.lib().fasmg_engine_kernels_per_vcycle(self.handle))
+
+
+class FasSolver:
+    """Reusable solver owning one workspace set per level (PKG/fas.py:63-89).
+
+    Workspaces live in the native engine (allocated on first use per
+    smoothing count ``s``), so time steppers that reuse a solver never
+    reallocate.
+    """
+
+    def __init__(self, hierarchy: GridHierarchy, location: Location,
+                 bc: BoundaryCondition, plan: SweepPlan, coeffs: OperatorCoeffs):
+        self.hierarchy = hierarchy
+        self.location = location
+        self.bc = bc
+        self.bc_homog = bc.homogenized()
+        self.plan = plan
+        self.coeffs = coeffs
+        self.use_graph = True
+        self._engines: dict = {}
+
+    def engine(self, s: int, device: torch.device) -> _Engine:
+        key = (int(s), device.index)
+        e = self._engines.get(key)
+        if e is None:
+            e = self._engines[key] = _Engine(self, s, device)
+        return e
+
+    def _check(self, p: Field, f: Field):
+        if p.location is not self.location or f.location is not self.location:
+            raise ValueError("field location does not match the solver")
+        if p.grid.shape != self.hierarchy.fine.shape or f.grid.shape != p.grid.shape:
+            raise ValueError("field grid does not match the solver hierarchy")
+
+    # -- one V-cycle -------------------------------------------------------
+    def vcycle(self, p: Field, f: Field, s: int) -> Field:
+        """One V-cycle on ``p`` in place (PKG/fas.py:93-128); leaves ghosts
+        stale."""
+        self._check(p, f)
+        e = self.engine(s, p.device)
+        e.load(p, f)
+        e.run(1, with_norm=False, use_graph=self.use_graph)
+        e.store(p)
+        p.ghosts_fresh = False
+        return p
+
+    # -- outer loop --------------------------------------------------------
+    def _singular(self) -> bool:
+        return self.coeffs.a == 0.0 and all(
+            rule.kind != "dirichlet" for _, rule in self.bc.faces)
+
+    def solve(self, p: Field, f: Field, params: FasParams) -> SolveReport:
+        """Iterate V-cycles on ``p`` until ``res <= tol`` (PKG/fas.py:137-162).
+        For a singular problem the rhs is shifted to zero mean in place and
+        the returned solution is shifted to zero mean."""
+        self._check(p, f)
+        singular = self._singular()
+        if singular:
+            subtract_interior_mean(f)
+        e = self.engine(params.s, p.device)
+        e.load(p, f)
+        g = self.hierarchy.fine
+        scale = g.h ** (g.dim / 2.0)
+        history: list = []
+        for _ in range(params.k_max):
+            sumsq = e.run(1, with_norm=True, use_graph=self.use_graph)
+            res = scale * math.sqrt(sumsq)
+            history.append(res)
+            if res <= params.tol:
+                break
+        e.store(p)
+        fill_ghosts(p, self.bc)
+        if singular:
+            subtract_interior_mean(p)
+            p.ghosts_fresh = False
+        return SolveReport(iterations=len(history), residual_history=history,
+                           converged=bool(history and history[-1] <= params.tol))
+
+
+def vcycle(p: Field, f: Field, coeffs: OperatorCoeffs, params: FasParams,
+           plan: SweepPlan, bc: BoundaryCondition, solver: FasSolver | None = None) -> Field:
+    """One V-cycle (PKG/fas.py:165-172)."""
+    if solver is None:
+        hier = make_hierarchy(p.grid, params.mesh_level)
+        solver = FasSolver(hier, p.location, bc, plan, coeffs)
+    return solver.vcycle(p, f, params.s)
+
+
+def solve(p0: Field, f: Field, coeffs: OperatorCoeffs, params: FasParams,
+          plan: SweepPlan, bc: BoundaryCondition):
+    """Solve ``a p - b Lap(p) = f`` from ``p0`` (updated in place)
+    (PKG/fas.py:175-181)."""
+    hier = make_hierarchy(p0.grid, params.mesh_level)
+    solver = FasSolver(hier, p0.location, bc, plan, coeffs)
+    report = solver.solve(p0, f, params)
+    return p0, report
