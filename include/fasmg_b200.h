@@ -142,6 +142,9 @@ int fasmg_engine_store(void* engine, double* pcore, const long* ps);
 int fasmg_engine_run(void* engine, int count, int with_norm, double* sumsq, int use_graph);
 int fasmg_engine_residual_sumsq(void* engine, double* sumsq);
 long fasmg_engine_kernels_per_vcycle(void* engine);
+/* mean duration (ms, CUDA events on the engine stream) of one smoothing
+ * half-sweep launch on `level`, over `reps` launches */
+int fasmg_engine_time_sweeps(void* engine, int level, int reps, double* ms);
 int fasmg_engine_level_info(void* engine, int level, long* info);
 
 #ifdef __cplusplus

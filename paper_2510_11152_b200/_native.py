@@ -54,6 +54,7 @@ _SIGS = {
     "fasmg_engine_run": "viiDi",
     "fasmg_engine_residual_sumsq": "vD",
     "fasmg_engine_level_info": "viL",
+    "fasmg_engine_time_sweeps": "viiD",
     "fasmg_stream_create": "V",
     "fasmg_stream_destroy": "v",
     "fasmg_stream_synchronize": "v",

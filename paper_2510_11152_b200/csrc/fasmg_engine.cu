@@ -18,10 +18,12 @@
 //
 // Ghosts.  The reference refills ghosts before every color
 // (PKG/smoothers.py:149).  A 5/7-point stencil reads a ghost only through
-// the single axis it crosses, and that ghost mirrors either the updated
-// point itself (Dirichlet 2v - p, Neumann copy), the opposite-parity wrap
-// (periodic) or a prescribed wall value, so every kernel evaluates ghosts
-// inline from current values -- bitwise identical, no ghost-fill launches.
+// the single axis it crosses, and that ghost mirrors either the point
+// itself (Dirichlet 2v - p, Neumann copy), the opposite-parity wrap
+// (periodic) or a prescribed wall value.  So each class array keeps its
+// ghost pads current: whichever kernel writes a boundary point also writes
+// the ghost derived from it (fasmg_stencil.cuh), every stencil load is
+// branch-free, and no ghost-fill launches are needed -- bitwise identical.
 // Edge-centered transfers, which read corner ghosts, use the full
 // fill-order chain (ghost_value in fasmg_common.cuh).
 //
@@ -35,8 +37,10 @@
 // graph and replayed per outer iteration.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "fasmg_common.cuh"
@@ -86,188 +90,9 @@ __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
     return !(qbit<D>(c, L.ea) == 0 && bb[L.ea] == L.B[L.ea]);
 }
 
-// Neighbor of point (c, bb) along `axis` in direction dir (+1/-1), with
-// the reference's ghost semantics evaluated inline.  `self` is the current
-// value of the point itself (needed only by Dirichlet/Neumann ghosts).
-template <int D>
-__device__ __forceinline__ double nbr(const double* P, const Lvl& L, const BcSpec& bc, int c,
-                                      const int* bb, int axis, int dir, const double* selfp) {
-    const int bit = 1 << (D - 1 - axis);
-    const int q = (c & bit) ? 1 : 0;
-    const int cn = c ^ bit;
-    int nb[3] = {bb[0], bb[1], bb[2]};
-    const int bn = bb[axis] + (q ? (dir > 0 ? 0 : -1) : (dir > 0 ? 1 : 0));
-    const bool edge = (axis == L.ea);
-    const int hi = (q == 1 && edge) ? L.B[axis] - 1 : L.B[axis];  // qn = 1 - q
-    if (bn >= 1 && bn <= hi) {
-        nb[axis] = bn;
-        return P[at<D>(L, cn, nb[0], nb[1], nb[2])];
-    }
-    const int side = dir > 0 ? 1 : 0;
-    const int kind = bc.kind[axis][side];
-    const double v = bc.val[axis][side];
-    if (kind == BC_NEUMANN) return *selfp;
-    if (!edge) {
-        if (kind == BC_DIRICHLET) return sb(ml(2.0, v), *selfp);
-        nb[axis] = dir < 0 ? L.B[axis] : 1;  // periodic wrap, same class cn
-        return P[at<D>(L, cn, nb[0], nb[1], nb[2])];
-    }
-    if (kind == BC_DIRICHLET) return v;
-    nb[axis] = 0;  // periodic edge axis: both walls hold the stored low wall
-    return P[at<D>(L, cn, nb[0], nb[1], nb[2])];
-}
-
-template <int D>
-__device__ __forceinline__ double nsum_at(const double* P, const Lvl& L, const BcSpec& bc,
-                                          int c, const int* bb, const double* selfp) {
-    // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:58-62)
-    double s = ad(nbr<D>(P, L, bc, c, bb, 0, +1, selfp), nbr<D>(P, L, bc, c, bb, 0, -1, selfp));
-    s = ad(s, nbr<D>(P, L, bc, c, bb, 1, +1, selfp));
-    s = ad(s, nbr<D>(P, L, bc, c, bb, 1, -1, selfp));
-    if (D == 3) {
-        s = ad(s, nbr<D>(P, L, bc, c, bb, 2, +1, selfp));
-        s = ad(s, nbr<D>(P, L, bc, c, bb, 2, -1, selfp));
-    }
-    return s;
-}
-
-// ------------------------------------------------------------- smoothing
-// One launch updates every class in `mask` (classes that are mutually
-// independent: equal index-sum parity).  Thread per block.
-template <int D>
-__global__ void __launch_bounds__(TPB) k_sweep(double* __restrict__ P,
-                                               const double* __restrict__ F, Lvl L,
-                                               BcSpec bc, unsigned mask) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= L.nblk) return;
-    int bb[3];
-    decode<D>(L, t, bb);
-    double out[1 << D];
-#pragma unroll
-    for (int c = 0; c < (1 << D); ++c) {
-        if (!(mask & (1u << c))) continue;
-        if (!interior<D>(L, c, bb)) continue;
-        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
-        double ns = nsum_at<D>(P, L, bc, c, bb, P + o);
-        out[c] = dv(ad(ml(L.h2, F[o]), ml(L.b, ns)), L.denom);
-    }
-#pragma unroll
-    for (int c = 0; c < (1 << D); ++c) {
-        if (!(mask & (1u << c))) continue;
-        if (!interior<D>(L, c, bb)) continue;
-        P[at<D>(L, c, bb[0], bb[1], bb[2])] = out[c];
-    }
-}
-
-// a*c - b*lap at one point (KER/numpy_backend.py:69-99)
-template <int D>
-__device__ __forceinline__ double op_at(const double* P, const Lvl& L, const BcSpec& bc, int c,
-                                        const int* bb, long o) {
-    const double cv = P[o];
-    double ns = nsum_at<D>(P, L, bc, c, bb, P + o);
-    double lap = ml(sb(ns, ml(D == 3 ? 6.0 : 4.0, cv)), L.inv_h2);
-    return sb(ml(L.a, cv), ml(L.b, lap));
-}
-
-// ----------------------------------------------------------- tau kernel
-// Cell-centered: residual at the 2^d children of coarse cell b, restriction
-// of r and p (lexicographic child order = descending class id,
-// KER/numba_backend.py:222-253), written to the coarse level's classes.
-template <int D>
-__global__ void __launch_bounds__(TPB) k_tau_cell(const double* __restrict__ P,
-                                                  const double* __restrict__ F, Lvl L,
-                                                  BcSpec bc, double* __restrict__ Pc,
-                                                  double* __restrict__ Fc, Lvl Lc) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= L.nblk) return;
-    int bb[3];
-    decode<D>(L, t, bb);
-    double rp = 0.0, rr = 0.0;
-#pragma unroll
-    for (int c = (1 << D) - 1; c >= 0; --c) {
-        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
-        const double pv = P[o];
-        const double r = sb(F[o], op_at<D>(P, L, bc, c, bb, o));
-        if (c == (1 << D) - 1) { rp = pv; rr = r; }
-        else { rp = ad(rp, pv); rr = ad(rr, r); }
-    }
-    const double sc = D == 3 ? 0.125 : 0.25;
-    // coarse cell index I = bb -> coarse class (I&1), block (I+1)>>1
-    int cc = 0, cb[3] = {0, 0, 0};
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-        cc |= (bb[a] & 1) << (D - 1 - a);
-        cb[a] = (bb[a] + 1) >> 1;
-    }
-    const long oc = at<D>(Lc, cc, cb[0], cb[1], cb[2]);
-    Pc[oc] = ml(rp, sc);
-    Fc[oc] = ml(rr, sc);
-}
-
-// f_c += a*p_c - b*Lap(p_c) on the coarse level (PKG/fas.py:107-110): full
-// BC ghosts on p_c.
-template <int D>
-__global__ void __launch_bounds__(TPB) k_coarse_src(const double* __restrict__ Pc,
-                                                    double* __restrict__ Fc, Lvl L, BcSpec bc) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= L.nblk) return;
-    int bb[3];
-    decode<D>(L, t, bb);
-#pragma unroll
-    for (int c = 0; c < (1 << D); ++c) {
-        if (!interior<D>(L, c, bb)) continue;
-        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
-        Fc[o] = ad(Fc[o], op_at<D>(Pc, L, bc, c, bb, o));
-    }
-}
-
-// Coarse correction, cell-centered (PKG/fas.py:119-123): c = p_c - R(p)
-// with R(p) recomputed from the unchanged fine p (equal to the stored
-// pinit), injected to the 2^d children and added.
-template <int D>
-__global__ void __launch_bounds__(TPB) k_correct_cell(double* __restrict__ P, Lvl L,
-                                                      const double* __restrict__ Pc, Lvl Lc) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= L.nblk) return;
-    int bb[3];
-    decode<D>(L, t, bb);
-    double pv[1 << D];
-    double rp = 0.0;
-#pragma unroll
-    for (int c = (1 << D) - 1; c >= 0; --c) {
-        pv[c] = P[at<D>(L, c, bb[0], bb[1], bb[2])];
-        rp = (c == (1 << D) - 1) ? pv[c] : ad(rp, pv[c]);
-    }
-    rp = ml(rp, D == 3 ? 0.125 : 0.25);
-    int cc = 0, cb[3] = {0, 0, 0};
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-        cc |= (bb[a] & 1) << (D - 1 - a);
-        cb[a] = (bb[a] + 1) >> 1;
-    }
-    const double corr = sb(Pc[at<D>(Lc, cc, cb[0], cb[1], cb[2])], rp);
-#pragma unroll
-    for (int c = 0; c < (1 << D); ++c) P[at<D>(L, c, bb[0], bb[1], bb[2])] = ad(pv[c], corr);
-}
+#include "fasmg_stencil.cuh"
 
 // ------------------------------------------------- edge-centered transfers
-// Residual into R (edge fields need it for the tangential stencil).
-template <int D>
-__global__ void __launch_bounds__(TPB) k_residual(const double* __restrict__ P,
-                                                  const double* __restrict__ F,
-                                                  double* __restrict__ R, Lvl L, BcSpec bc) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= L.nblk) return;
-    int bb[3];
-    decode<D>(L, t, bb);
-#pragma unroll
-    for (int c = 0; c < (1 << D); ++c) {
-        if (!interior<D>(L, c, bb)) continue;
-        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
-        R[o] = sb(F[o], op_at<D>(P, L, bc, c, bb, o));
-    }
-}
-
 // Reader of raw stored values at core (grid) index x in the blocked layout.
 template <int D>
 struct BlkReader {
@@ -483,39 +308,6 @@ __global__ void __launch_bounds__(TPB) k_correct_edge(double* __restrict__ P, Lv
     }
 }
 
-// ------------------------------------------------- outer residual norm
-// sum over interior points of r^2 with r = f - (a p - b Lap p); per-CTA
-// partial sums in a fixed tree order, then a single-CTA fixed-order final
-// reduction (deterministic, run-to-run stable).
-template <int D>
-__global__ void __launch_bounds__(TPB) k_res_sumsq(const double* __restrict__ P,
-                                                   const double* __restrict__ F, Lvl L,
-                                                   BcSpec bc, double* __restrict__ part) {
-    __shared__ double sh[TPB / 32];
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    double acc = 0.0;
-    if (t < L.nblk) {
-        int bb[3];
-        decode<D>(L, t, bb);
-#pragma unroll
-        for (int c = 0; c < (1 << D); ++c) {
-            if (!interior<D>(L, c, bb)) continue;
-            const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
-            const double r = sb(F[o], op_at<D>(P, L, bc, c, bb, o));
-            acc = ad(acc, ml(r, r));
-        }
-    }
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) acc = ad(acc, __shfl_down_sync(0xffffffffu, acc, s));
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = sh[0];
-        for (int w = 1; w < TPB / 32; ++w) s = ad(s, sh[w]);
-        part[blockIdx.x] = s;
-    }
-}
-
 __global__ void k_final_sum(const double* __restrict__ part, int n, double* out) {
     __shared__ double sh[1024];
     double acc = 0.0;
@@ -607,14 +399,144 @@ struct Engine {
     cudaGraph_t graph_v = nullptr, graph_vn = nullptr;
     cudaGraphExec_t exec_v = nullptr, exec_vn = nullptr;
     long kernels_per_vcycle = 0;
+    int sweep_variant = 0;  // 0: thread per block, 1: per (block, class), 2: 2.5D march
+    int march_chunk = 32;   // planes per marching chunk
 };
+
+struct Tile {
+    dim3 grid, block;
+};
+
+static unsigned p2ceil(unsigned v) {
+    unsigned r = 1;
+    while (r < v) r <<= 1;
+    return r;
+}
+
+// thread block shape over (b2, b1, b0) [3D] or (b1, b0) [2D]
+static unsigned g_tile_y = 8;  // FASMG_TILE_Y: rows of b1 per CTA (3D)
+
+static Tile tile_of(const Lvl& L) {
+    Tile t;
+    if (L.dim == 3) {
+        unsigned bx = std::min(32u, p2ceil(L.B[2]));
+        unsigned by = std::min(std::min(g_tile_y, 256u / bx), p2ceil(L.B[1]));
+        unsigned bz = std::min(256u / (bx * by), p2ceil(L.B[0]));
+        t.block = dim3(bx, by, bz);
+        t.grid = dim3((L.B[2] + bx - 1) / bx, (L.B[1] + by - 1) / by, (L.B[0] + bz - 1) / bz);
+    } else {
+        unsigned bx = std::min(64u, p2ceil(L.B[1]));
+        unsigned by = std::min(256u / bx, p2ceil(L.B[0]));
+        t.block = dim3(bx, by, 1);
+        t.grid = dim3((L.B[1] + bx - 1) / bx, (L.B[0] + by - 1) / by, 1);
+    }
+    return t;
+}
+
+static inline long tile_ctas(const Tile& t) { return (long)t.grid.x * t.grid.y * t.grid.z; }
+
+// class masks the sweep kernel is instantiated for: all odd / all even
+// index-sum classes (X and RBGS plans) and single classes (U/Z plans)
+static bool mask_supported(int dim, unsigned m) {
+    unsigned odd = dim == 3 ? 0x96u : 0x6u, even = dim == 3 ? 0x69u : 0x9u;
+    if (m == odd || m == even) return true;
+    return m != 0 && (m & (m - 1)) == 0 && m < (1u << (1 << dim));
+}
+
+template <int D, int EA, unsigned M>
+static void sweep_one(Engine& E, int k, const Tile& t) {
+    const Lvl& L = E.L[k];
+    if (E.sweep_variant == 1) {
+        constexpr int NCM = __builtin_popcount(M);
+        dim3 blk, grd;
+        if (D == 3) {
+            unsigned bx = std::min(32u, p2ceil(L.B[2]));
+            unsigned by = std::min(256u / bx, p2ceil(L.B[1]));
+            blk = dim3(bx, by, 1);
+            grd = dim3((L.B[2] + bx - 1) / bx, (L.B[1] + by - 1) / by, L.B[0] * NCM);
+        } else {
+            unsigned bx = std::min(64u, p2ceil(L.B[1]));
+            unsigned by = std::min(256u / bx, p2ceil(L.B[0]));
+            blk = dim3(bx, by, 1);
+            grd = dim3((L.B[1] + bx - 1) / bx, (L.B[0] + by - 1) / by, NCM);
+        }
+        k_sweep_pc<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
+        return;
+    }
+    if (E.sweep_variant == 2 && __builtin_popcount(M) > 1) {
+        const int chunk = E.march_chunk;
+        dim3 blk, grd;
+        const unsigned nch = (L.B[0] + chunk - 1) / chunk;
+        if (D == 3) {
+            unsigned bx = std::min(32u, p2ceil(L.B[2]));
+            unsigned by = std::min(256u / bx, p2ceil(L.B[1]));
+            blk = dim3(bx, by, 1);
+            grd = dim3((L.B[2] + bx - 1) / bx, (L.B[1] + by - 1) / by, nch);
+        } else {
+            unsigned bx = std::min(256u, p2ceil(L.B[1]));
+            blk = dim3(bx, 1, 1);
+            grd = dim3((L.B[1] + bx - 1) / bx, nch, 1);
+        }
+        k_sweep_march<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
+        return;
+    }
+    k_sweep_fast<D, EA, M><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
+}
+
+template <int D, int EA>
+static void sweep_mask(Engine& E, int k, unsigned m, const Tile& t) {
+    if (D == 3) {
+        switch (m) {
+            case 0x96u: sweep_one<D, EA, 0x96u>(E, k, t); return;
+            case 0x69u: sweep_one<D, EA, 0x69u>(E, k, t); return;
+            case 0x01u: sweep_one<D, EA, 0x01u>(E, k, t); return;
+            case 0x02u: sweep_one<D, EA, 0x02u>(E, k, t); return;
+            case 0x04u: sweep_one<D, EA, 0x04u>(E, k, t); return;
+            case 0x08u: sweep_one<D, EA, 0x08u>(E, k, t); return;
+            case 0x10u: sweep_one<D, EA, 0x10u>(E, k, t); return;
+            case 0x20u: sweep_one<D, EA, 0x20u>(E, k, t); return;
+            case 0x40u: sweep_one<D, EA, 0x40u>(E, k, t); return;
+            case 0x80u: sweep_one<D, EA, 0x80u>(E, k, t); return;
+        }
+    } else {
+        switch (m) {
+            case 0x6u: sweep_one<D, EA, 0x6u>(E, k, t); return;
+            case 0x9u: sweep_one<D, EA, 0x9u>(E, k, t); return;
+            case 0x1u: sweep_one<D, EA, 0x1u>(E, k, t); return;
+            case 0x2u: sweep_one<D, EA, 0x2u>(E, k, t); return;
+            case 0x4u: sweep_one<D, EA, 0x4u>(E, k, t); return;
+            case 0x8u: sweep_one<D, EA, 0x8u>(E, k, t); return;
+        }
+    }
+}
+
+// dispatch the runtime edge axis onto the compile-time one
+#define EA_DISPATCH(D, EAV, CALL)                              \
+    do {                                                       \
+        switch (EAV) {                                         \
+            case -1: { constexpr int EA = -1; CALL; } break;   \
+            case 0: { constexpr int EA = 0; CALL; } break;     \
+            case 1: { constexpr int EA = 1; CALL; } break;     \
+            default: { constexpr int EA = (D == 3 ? 2 : 1); CALL; } break; \
+        }                                                      \
+    } while (0)
+
+template <int D>
+static void launch_pad_fill(Engine& E, int k, long& cnt) {
+    const Lvl& L = E.L[k];
+    long face = 1;
+    for (int a = 0; a < D; ++a) face = std::max(face, L.nblk / L.B[a]);
+    dim3 grid(nb(face, 128), 2 * D);
+    EA_DISPATCH(D, E.ea, (k_pad_fill<D, EA><<<grid, 128, 0, E.stream>>>(E.P[k], L, E.bc)));
+    ++cnt;
+}
 
 template <int D>
 static void launch_smooth(Engine& E, int k, long& cnt) {
-    const Lvl& L = E.L[k];
+    const Tile t = tile_of(E.L[k]);
     for (int it = 0; it < E.s; ++it)
         for (unsigned m : E.masks) {
-            k_sweep<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, m);
+            EA_DISPATCH(D, E.ea, (sweep_mask<D, EA>(E, k, m, t)));
             ++cnt;
         }
 }
@@ -625,14 +547,15 @@ static void launch_vcycle(Engine& E, long& cnt) {
     for (int k = 0; k < E.nl - 1; ++k) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
+        const Tile t = tile_of(L), tc = tile_of(Lc);
         launch_smooth<D>(E, k, cnt);
         if (E.ea < 0) {
-            k_tau_cell<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc,
-                                                                 E.P[k + 1], E.F[k + 1], Lc);
+            k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.P[k + 1],
+                                                             E.F[k + 1], Lc, E.bc);
             ++cnt;
         } else {
-            k_residual<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], E.F[k], E.R[k], L,
-                                                                 E.bc);
+            EA_DISPATCH(D, E.ea, (k_residual_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
+                                     E.P[k], E.F[k], E.R[k], L)));
             long mc = 1;
             for (int a = 0; a < D; ++a) mc *= (a == E.ea ? Lc.n[a] - 1 : Lc.n[a]);
             k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.bc, E.P[k + 1],
@@ -642,9 +565,10 @@ static void launch_vcycle(Engine& E, long& cnt) {
             long tot = Lc.cls * (1 << D);
             k_copy_blk<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], tot);
             cnt += 4;
+            launch_pad_fill<D>(E, k + 1, cnt);
         }
-        k_coarse_src<D><<<nb(Lc.nblk, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.F[k + 1], Lc,
-                                                                E.bc);
+        EA_DISPATCH(D, E.ea, (k_coarse_src_fast<D, EA><<<tc.grid, tc.block, 0, E.stream>>>(
+                                 E.P[k + 1], E.F[k + 1], Lc)));
         ++cnt;
     }
     launch_smooth<D>(E, E.nl - 1, cnt);  // coarsest: s smoothing steps
@@ -652,12 +576,16 @@ static void launch_vcycle(Engine& E, long& cnt) {
     for (int k = E.nl - 2; k >= 0; --k) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
-        if (E.ea < 0)
-            k_correct_cell<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc);
-        else
+        const Tile t = tile_of(L);
+        if (E.ea < 0) {
+            k_correct_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc, E.bc);
+            ++cnt;
+        } else {
             k_correct_edge<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1],
                                                                      E.PI[k + 1], Lc, E.bch);
-        ++cnt;
+            ++cnt;
+            launch_pad_fill<D>(E, k, cnt);
+        }
         launch_smooth<D>(E, k, cnt);
     }
 }
@@ -665,7 +593,9 @@ static void launch_vcycle(Engine& E, long& cnt) {
 template <int D>
 static void launch_norm(Engine& E, long& cnt) {
     const Lvl& L = E.L[0];
-    k_res_sumsq<D><<<E.npart, TPB, 0, E.stream>>>(E.P[0], E.F[0], L, E.bc, E.part);
+    const Tile t = tile_of(L);
+    EA_DISPATCH(D, E.ea, (k_res_sumsq_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
+                             E.P[0], E.F[0], L, E.part)));
     k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, E.npart, E.dsum);
     cnt += 2;
 }
@@ -763,7 +693,16 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
             E->bch.kind[t][sd] = E->bc.kind[t][sd];
             E->bch.val[t][sd] = 0.0;  // PKG/boundary.py:83-87
         }
+    for (int t = 0; t < nmasks; ++t)
+        if (!mask_supported(dim, masks[t])) {
+            fasmg_set_error(FASMG_EINVAL, "unsupported class mask in smoothing plan");
+            delete E;
+            return nullptr;
+        }
     E->masks.assign(masks, masks + nmasks);
+    if (const char* v = getenv("FASMG_SWEEP_VARIANT")) E->sweep_variant = atoi(v);
+    if (const char* v = getenv("FASMG_MARCH_CHUNK")) E->march_chunk = std::max(1, atoi(v));
+    if (const char* v = getenv("FASMG_TILE_Y")) g_tile_y = std::max(1, atoi(v));
     int nn[3] = {n[0], n[1], dim == 3 ? n[2] : 2};
     for (int k = 0; k < E->nl; ++k) {
         E->L[k] = make_lvl(dim, nn, ea, dmin, dmax, a, b);
@@ -782,7 +721,7 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
         }
         for (int t = 0; t < dim; ++t) nn[t] /= 2;
     }
-    E->npart = nb(E->L[0].nblk, TPB);
+    E->npart = (int)tile_ctas(tile_of(E->L[0]));
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
         fasmg_check(cudaMallocHost(&E->hsum, sizeof(double)))) {
@@ -832,6 +771,9 @@ int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double
         k_pack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(fcore, fs[0], fs[1], 0, E->F[0], L, e[0],
                                                         e[1], 1);
     }
+    long cnt = 0;
+    if (E->dim == 3) launch_pad_fill<3>(*E, 0, cnt);
+    else launch_pad_fill<2>(*E, 0, cnt);
     return fasmg_check_launch();
 }
 
@@ -895,6 +837,34 @@ int fasmg_engine_residual_sumsq(void* h, double* sumsq) {
     int st = fasmg_check(cudaStreamSynchronize(E->stream));
     if (!st) *sumsq = *E->hsum;
     return st;
+}
+
+// Time `reps` smoothing half-sweep launches of level k (the smoother's
+// masks in order, cycling) with CUDA events on the engine stream; returns
+// the mean duration of one launch in *ms.  This is the live per-launch
+// timing bench.py reports for the roofline.
+int fasmg_engine_time_sweeps(void* h, int k, int reps, double* ms) {
+    Engine* E = (Engine*)h;
+    if (k < 0 || k >= E->nl || reps < 1) return fasmg_set_error(FASMG_EINVAL, "bad level/reps");
+    cudaEvent_t a, b;
+    int st = fasmg_check(cudaEventCreate(&a));
+    if (st) return st;
+    if ((st = fasmg_check(cudaEventCreate(&b)))) { cudaEventDestroy(a); return st; }
+    const Tile t = tile_of(E->L[k]);
+    cudaEventRecord(a, E->stream);
+    for (int r = 0; r < reps; ++r) {
+        unsigned m = E->masks[r % E->masks.size()];
+        if (E->dim == 3) EA_DISPATCH(3, E->ea, (sweep_mask<3, EA>(*E, k, m, t)));
+        else EA_DISPATCH(2, E->ea, (sweep_mask<2, EA>(*E, k, m, t)));
+    }
+    cudaEventRecord(b, E->stream);
+    st = fasmg_check(cudaEventSynchronize(b));
+    float f = 0.f;
+    if (!st) st = fasmg_check(cudaEventElapsedTime(&f, a, b));
+    *ms = f / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return st ? st : fasmg_check_launch();
 }
 
 long fasmg_engine_kernels_per_vcycle(void* h) { return ((Engine*)h)->kernels_per_vcycle; }

@@ -1,0 +1,532 @@
+// fasmg_stencil.cuh -- branch-free stencil kernels on the parity-blocked
+// layout (included by fasmg_engine.cu, which defines Lvl/at/qbit).
+//
+// Ghost pads.  Every class array carries pad blocks 0 and B+1 per axis.  A
+// 5/7-point stencil reads a ghost only as the neighbor of the one interior
+// point it mirrors, so the pad slot of each boundary point's ghost (and the
+// edge-axis wall slots) are kept current: the kernel that writes a
+// boundary point also writes the ghost value the reference's fill_ghosts
+// would produce from it (PKG/boundary.py:110-156):
+//   cell axis   lo ghost (x=0)   : dirichlet 2v - p(1), neumann p(1),
+//                                  periodic p(n)
+//               hi ghost (x=n+1) : dirichlet 2v - p(n), neumann p(n),
+//                                  periodic p(1)
+//   edge axis   lo wall (x=0)    : dirichlet v, neumann p(1), periodic the
+//                                  stored wall (never written)
+//               hi wall (x=n)    : dirichlet v, neumann p(n-1), periodic =
+//                                  lo wall
+// In the blocked layout these are exactly the slots a branch-free neighbor
+// load hits: W of (q=1, b=1) is (q=0, b=0); E of (q=0, b=B) is (q=1, b=B+1);
+// E of the edge point (q=1, b=B) is the wall slot (q=0, b=B).  A pad slot is
+// only ever read by the point it mirrors, so a kernel may write it in the
+// same launch after that thread's own loads.
+#pragma once
+
+// (included inside namespace fasmg)
+
+// linear strides of the block axes
+template <int D>
+__device__ __forceinline__ long bstride(const Lvl& L, int a) {
+    if (D == 3) return a == 0 ? L.s0 : (a == 1 ? L.s1 : 1);
+    return a == 0 ? L.s0 : 1;
+}
+
+// 3D-block thread mapping: x -> last block axis, y -> next, z -> axis 0.
+template <int D>
+__device__ __forceinline__ bool tile_coords(const Lvl& L, int* bb) {
+    if (D == 3) {
+        bb[2] = blockIdx.x * blockDim.x + threadIdx.x + 1;
+        bb[1] = blockIdx.y * blockDim.y + threadIdx.y + 1;
+        bb[0] = blockIdx.z * blockDim.z + threadIdx.z + 1;
+        return bb[0] <= L.B[0] && bb[1] <= L.B[1] && bb[2] <= L.B[2];
+    }
+    bb[1] = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    bb[0] = blockIdx.y * blockDim.y + threadIdx.y + 1;
+    bb[2] = 0;
+    return bb[0] <= L.B[0] && bb[1] <= L.B[1];
+}
+
+template <int D>
+__device__ __forceinline__ bool on_boundary(const Lvl& L, const int* bb) {
+    bool r = false;
+#pragma unroll
+    for (int a = 0; a < D; ++a) r = r || bb[a] == 1 || bb[a] == L.B[a];
+    return r;
+}
+
+// edge-axis wall position of class c at block bb (not an unknown)
+template <int D, int EA>
+__device__ __forceinline__ bool is_wall(const Lvl& L, int c, const int* bb) {
+    if (EA < 0) return false;
+    return qbit<D>(c, EA) == 0 && bb[EA] == L.B[EA];
+}
+
+// sum of the 2d neighbors of point (c, o) in the reference order
+// ((((E+W)+N)+S)+T)+B, all through (pad-backed) branch-free loads.
+template <int D>
+__device__ __forceinline__ double nsum_fast(const double* __restrict__ P, const Lvl& L, int c,
+                                            long o) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int bit = 1 << (D - 1 - a);
+        const long dcls = (long)((c ^ bit) - c) * L.cls;
+        const long sa = bstride<D>(L, a);
+        const bool q = (c & bit) != 0;
+        const double e = P[o + dcls + (q ? 0 : sa)];
+        const double w = P[o + dcls - (q ? sa : 0)];
+        s = (a == 0) ? ad(e, w) : ad(ad(s, e), w);
+    }
+    return s;
+}
+
+// After writing value v at boundary point (c, bb) (offset o), refresh the
+// ghost / wall slots derived from it.
+template <int D, int EA>
+__device__ __forceinline__ void write_pads(double* __restrict__ P, const Lvl& L,
+                                           const BcSpec& bc, int c, const int* bb, long o,
+                                           double v) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int bit = 1 << (D - 1 - a);
+        const long dcls = (long)((c ^ bit) - c) * L.cls;
+        const long sa = bstride<D>(L, a);
+        const bool q = (c & bit) != 0;
+        const int B = L.B[a];
+        if (a != EA) {
+            if (q && bb[a] == 1) {
+                const int k = bc.kind[a][0];
+                if (k == BC_DIRICHLET) P[o + dcls - sa] = sb(ml(2.0, bc.val[a][0]), v);
+                else if (k == BC_NEUMANN) P[o + dcls - sa] = v;
+                else P[o + (long)B * sa] = v;  // periodic: hi ghost x=n+1 <- p(1)
+            }
+            if (!q && bb[a] == B) {
+                const int k = bc.kind[a][1];
+                if (k == BC_DIRICHLET) P[o + dcls + sa] = sb(ml(2.0, bc.val[a][1]), v);
+                else if (k == BC_NEUMANN) P[o + dcls + sa] = v;
+                else P[o - (long)B * sa] = v;  // periodic: lo ghost x=0 <- p(n)
+            }
+        } else {
+            if (q && bb[a] == 1 && bc.kind[a][0] == BC_NEUMANN) P[o + dcls - sa] = v;
+            if (q && bb[a] == B && bc.kind[a][1] == BC_NEUMANN) P[o + dcls] = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------- pad fill
+// Initialize every pad/wall slot of a level from its interior (after a
+// pack, a restriction or an edge correction).  Launch: grid.y = face id
+// (2*D faces), x over the face's blocks.
+template <int D, int EA>
+__global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
+    const int face = blockIdx.y;
+    const int a = face >> 1, side = face & 1;
+    // enumerate the other axes' blocks
+    int oth[2], no = 0;
+#pragma unroll
+    for (int t = 0; t < D; ++t)
+        if (t != a) oth[no++] = t;
+    long n1 = L.B[oth[0]], n2 = (D == 3) ? L.B[oth[1]] : 1;
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n1 * n2) return;
+    int bb[3] = {0, 0, 0};
+    bb[a] = side ? L.B[a] : 1;
+    if (D == 3) {
+        bb[oth[1]] = 1 + (int)(t % n2);
+        bb[oth[0]] = 1 + (int)(t / n2);
+    } else {
+        bb[oth[0]] = 1 + (int)t;
+    }
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        const long o = o0 + (long)c * L.cls;
+        if (EA >= 0 && a == EA && qbit<D>(c, EA) == 0) {
+            const long sa = bstride<D>(L, EA);
+            // constant walls of this class at this face
+            if (side == 0) {
+                if (bc.kind[EA][0] == BC_DIRICHLET) P[o - sa] = bc.val[EA][0];
+            } else {
+                // o is the hi wall slot itself (q=0, b=B)
+                if (bc.kind[EA][1] == BC_DIRICHLET) P[o] = bc.val[EA][1];
+                else if (bc.kind[EA][1] == BC_PERIODIC) P[o] = P[o - (long)L.B[EA] * sa];
+            }
+        }
+        if (is_wall<D, EA>(L, c, bb)) continue;
+        write_pads<D, EA>(P, L, bc, c, bb, o, P[o]);
+    }
+}
+
+// ------------------------------------------------------------- smoothing
+// One launch = the reference's colors whose classes are in MASK (mutually
+// independent classes; PKG/smoothers.py:136-153).  Thread per block.
+template <int D, int EA, unsigned MASK>
+__global__ void __launch_bounds__(256) k_sweep_fast(double* __restrict__ P,
+                                                    const double* __restrict__ F, Lvl L,
+                                                    BcSpec bc) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+    constexpr int NC = 1 << D;
+    // phase 1: issue every load of every class before any arithmetic, so
+    // the division's slow-path call cannot serialize them
+    double nbv[NC][2 * D], fv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (!((MASK >> c) & 1u)) continue;
+        const long o = o0 + (long)c * L.cls;
+        fv[c] = F[o];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int bit = 1 << (D - 1 - a);
+            const long dcls = (long)((c ^ bit) - c) * L.cls;
+            const long sa = bstride<D>(L, a);
+            const bool q = (c & bit) != 0;
+            // opposite-parity classes are not written by this launch except
+            // pad slots only this thread reads (before writing): the
+            // non-coherent read-only path is safe
+            nbv[c][2 * a] = __ldg(P + o + dcls + (q ? 0 : sa));
+            nbv[c][2 * a + 1] = __ldg(P + o + dcls - (q ? sa : 0));
+        }
+    }
+    // phase 2: numerators h2*f + b*((((E+W)+N)+S)+T)+B for every class first
+    // (so the loaded values are dead before any division's slow-path call),
+    // then the IEEE divisions by denom (KER/numpy_backend.py:44,62)
+    double nv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (!((MASK >> c) & 1u)) continue;
+        double ns = ad(nbv[c][0], nbv[c][1]);
+#pragma unroll
+        for (int t = 2; t < 2 * D; ++t) ns = ad(ns, nbv[c][t]);
+        nv[c] = ad(ml(L.h2, fv[c]), ml(L.b, ns));
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+    const bool bnd = on_boundary<D>(L, bb);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (!((MASK >> c) & 1u)) continue;
+        if (is_wall<D, EA>(L, c, bb)) continue;
+        const long o = o0 + (long)c * L.cls;
+        P[o] = nv[c];
+        if (bnd) write_pads<D, EA>(P, L, bc, c, bb, o, nv[c]);
+    }
+}
+
+// Same update, one thread per (block, class): grid.z enumerates (b0, k-th
+// class of MASK) [3D] / (k-th class) [2D].  Fewer registers per thread and
+// one division each, so many more warps are resident to hide DRAM latency;
+// the classes of one block share their loads through L1/L2.
+template <int D, unsigned MASK>
+__device__ __forceinline__ int mask_class(int k) {
+    int n = 0;
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c)
+        if ((MASK >> c) & 1u) {
+            if (n == k) return c;
+            ++n;
+        }
+    return 0;
+}
+
+template <int D, int EA, unsigned MASK>
+__global__ void __launch_bounds__(256) k_sweep_pc(double* __restrict__ P,
+                                                  const double* __restrict__ F, Lvl L,
+                                                  BcSpec bc) {
+    constexpr int NCM = __builtin_popcount(MASK);
+    int bb[3], kc;
+    if (D == 3) {
+        bb[2] = blockIdx.x * blockDim.x + threadIdx.x + 1;
+        bb[1] = blockIdx.y * blockDim.y + threadIdx.y + 1;
+        bb[0] = blockIdx.z / NCM + 1;
+        kc = blockIdx.z % NCM;
+        if (bb[1] > L.B[1] || bb[2] > L.B[2]) return;
+    } else {
+        bb[1] = blockIdx.x * blockDim.x + threadIdx.x + 1;
+        bb[0] = blockIdx.y * blockDim.y + threadIdx.y + 1;
+        bb[2] = 0;
+        kc = blockIdx.z;
+        if (bb[0] > L.B[0] || bb[1] > L.B[1]) return;
+    }
+    const int c = mask_class<D, MASK>(kc);
+    if (is_wall<D, EA>(L, c, bb)) return;
+    const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+    double nbv[2 * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int bit = 1 << (D - 1 - a);
+        const long dcls = (long)((c ^ bit) - c) * L.cls;
+        const long sa = bstride<D>(L, a);
+        const bool q = (c & bit) != 0;
+        nbv[2 * a] = P[o + dcls + (q ? 0 : sa)];
+        nbv[2 * a + 1] = P[o + dcls - (q ? sa : 0)];
+    }
+    const double fv = F[o];
+    double ns = ad(nbv[0], nbv[1]);
+#pragma unroll
+    for (int t = 2; t < 2 * D; ++t) ns = ad(ns, nbv[t]);
+    const double v = dv(ad(ml(L.h2, fv), ml(L.b, ns)), L.denom);
+    P[o] = v;
+    if (on_boundary<D>(L, bb)) write_pads<D, EA>(P, L, bc, c, bb, o, v);
+}
+
+// 2.5D marching half-sweep.  Each thread owns one column of blocks along
+// axis 0 (a chunk of planes) and keeps, for every opposite-parity class k, a
+// two-plane register window of its values along axis 0: classes with
+// q0(k)=0 hold planes (b0-1, b0), classes with q0(k)=1 hold (b0, b0+1) --
+// exactly the W/E neighbors along axis 0 of the updated classes.  The next
+// plane of the window and of f is prefetched one step ahead, so every warp
+// keeps independent DRAM loads in flight across the whole column.  Axis-1/2
+// neighbors come from L1 (loaded as window values by neighboring threads).
+template <int D>
+__host__ __device__ constexpr unsigned opp_mask(unsigned m) {
+    unsigned r = 0;
+    for (int c = 0; c < (1 << D); ++c)
+        if ((m >> c) & 1u)
+            for (int a = 0; a < D; ++a) r |= 1u << (c ^ (1 << (D - 1 - a)));
+    return r;
+}
+
+template <int D, int EA, unsigned MASK>
+__global__ void __launch_bounds__(256) k_sweep_march(double* __restrict__ P,
+                                                     const double* __restrict__ F, Lvl L,
+                                                     BcSpec bc, int chunk) {
+    constexpr int NC = 1 << D;
+    constexpr unsigned OPP = opp_mask<D>(MASK);
+    constexpr int BIT0 = 1 << (D - 1);
+    int bb[3];
+    int z;
+    if (D == 3) {
+        bb[2] = blockIdx.x * blockDim.x + threadIdx.x + 1;
+        bb[1] = blockIdx.y * blockDim.y + threadIdx.y + 1;
+        z = blockIdx.z;
+        if (bb[1] > L.B[1] || bb[2] > L.B[2]) return;
+    } else {
+        bb[1] = blockIdx.x * blockDim.x + threadIdx.x + 1;
+        bb[2] = 0;
+        z = blockIdx.y;
+        if (bb[1] > L.B[1]) return;
+    }
+    const int b0s = 1 + z * chunk;
+    const int b0e = min(L.B[0], b0s + chunk - 1);
+    const long s0 = L.s0;
+    const long col = at<D>(L, 0, 0, bb[1], bb[2]);  // class 0, plane 0
+    bool bnd_col = false;
+#pragma unroll
+    for (int a = 1; a < D; ++a) bnd_col = bnd_col || bb[a] == 1 || bb[a] == L.B[a];
+
+    double w0[NC], w1[NC], wn[NC], fv[NC], fn[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        if (!((OPP >> k) & 1u)) continue;
+        const long ok = col + (long)k * L.cls;
+        const int lo = (k & BIT0) ? b0s : b0s - 1;
+        w0[k] = P[ok + (long)lo * s0];
+        w1[k] = P[ok + (long)(lo + 1) * s0];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if ((MASK >> c) & 1u) fv[c] = F[col + (long)c * L.cls + (long)b0s * s0];
+
+    for (int b0 = b0s; b0 <= b0e; ++b0) {
+        const bool more = b0 < b0e;
+        if (more) {  // prefetch the next step's window plane and f
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                if (!((OPP >> k) & 1u)) continue;
+                const int nxt = (k & BIT0) ? b0 + 2 : b0 + 1;
+                wn[k] = P[col + (long)k * L.cls + (long)nxt * s0];
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if ((MASK >> c) & 1u) fn[c] = F[col + (long)c * L.cls + (long)(b0 + 1) * s0];
+        }
+        bb[0] = b0;
+        const long pl = col + (long)b0 * s0;
+        double nv[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            if (!((MASK >> c) & 1u)) continue;
+            const int k0 = c ^ BIT0;
+            // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:44,62)
+            double ns = ad(w1[k0], w0[k0]);
+#pragma unroll
+            for (int a = 1; a < D; ++a) {
+                const int bit = 1 << (D - 1 - a);
+                const long sa = bstride<D>(L, a);
+                const bool q = (c & bit) != 0;
+                const long ok = pl + (long)(c ^ bit) * L.cls;
+                const double e = P[ok + (q ? 0 : sa)];
+                const double w = P[ok - (q ? sa : 0)];
+                ns = ad(ad(ns, e), w);
+            }
+            nv[c] = dv(ad(ml(L.h2, fv[c]), ml(L.b, ns)), L.denom);
+        }
+        const bool bnd = bnd_col || b0 == 1 || b0 == L.B[0];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            if (!((MASK >> c) & 1u)) continue;
+            if (is_wall<D, EA>(L, c, bb)) continue;
+            const long o = pl + (long)c * L.cls;
+            P[o] = nv[c];
+            if (bnd) write_pads<D, EA>(P, L, bc, c, bb, o, nv[c]);
+        }
+        if (more) {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                if (!((OPP >> k) & 1u)) continue;
+                w0[k] = w1[k];
+                w1[k] = wn[k];
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if ((MASK >> c) & 1u) fv[c] = fn[c];
+        }
+    }
+}
+
+// a*c - b*((nsum - 2d c) * inv_h2) at (c, o)  (KER/numpy_backend.py:69-99)
+template <int D>
+__device__ __forceinline__ double op_fast(const double* __restrict__ P, const Lvl& L, int c,
+                                          long o) {
+    const double cv = P[o];
+    const double ns = nsum_fast<D>(P, L, c, o);
+    const double lap = ml(sb(ns, ml(D == 3 ? 6.0 : 4.0, cv)), L.inv_h2);
+    return sb(ml(L.a, cv), ml(L.b, lap));
+}
+
+// ----------------------------------------------------------- tau kernel
+// Cell-centered fine level k -> coarse level k+1 in one pass: residual at the
+// 2^d children of coarse cell bb, restriction of r and p (lexicographic child
+// order = descending class id, KER/numba_backend.py:222-253), stored into the
+// coarse level's blocked arrays with its ghost pads (full BC on p_c,
+// PKG/fas.py:99-107).
+template <int D>
+__global__ void __launch_bounds__(256) k_tau_fast(const double* __restrict__ P,
+                                                  const double* __restrict__ F, Lvl L,
+                                                  double* __restrict__ Pc,
+                                                  double* __restrict__ Fc, Lvl Lc, BcSpec bc) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+    double rp = 0.0, rr = 0.0;
+#pragma unroll
+    for (int c = (1 << D) - 1; c >= 0; --c) {
+        const long o = o0 + (long)c * L.cls;
+        const double pv = P[o];
+        const double r = sb(F[o], op_fast<D>(P, L, c, o));
+        if (c == (1 << D) - 1) { rp = pv; rr = r; }
+        else { rp = ad(rp, pv); rr = ad(rr, r); }
+    }
+    const double sc = D == 3 ? 0.125 : 0.25;
+    int cc = 0, cb[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        cc |= (bb[a] & 1) << (D - 1 - a);
+        cb[a] = (bb[a] + 1) >> 1;
+    }
+    const long oc = at<D>(Lc, cc, cb[0], cb[1], cb[2]);
+    const double pcv = ml(rp, sc);
+    Pc[oc] = pcv;
+    Fc[oc] = ml(rr, sc);
+    if (on_boundary<D>(Lc, cb)) write_pads<D, -1>(Pc, Lc, bc, cc, cb, oc, pcv);
+}
+
+// f_c += a*p_c - b*Lap(p_c) on the coarse level (PKG/fas.py:108-110)
+template <int D, int EA>
+__global__ void __launch_bounds__(256) k_coarse_src_fast(const double* __restrict__ Pc,
+                                                         double* __restrict__ Fc, Lvl L) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (is_wall<D, EA>(L, c, bb)) continue;
+        const long o = o0 + (long)c * L.cls;
+        Fc[o] = ad(Fc[o], op_fast<D>(Pc, L, c, o));
+    }
+}
+
+// Cell-centered coarse correction (PKG/fas.py:119-123): c = p_c - R(p), R(p)
+// recomputed from the unchanged fine p (equals the reference's pinit),
+// injected and added; refreshes the fine ghost pads.
+template <int D>
+__global__ void __launch_bounds__(256) k_correct_fast(double* __restrict__ P, Lvl L,
+                                                      const double* __restrict__ Pc, Lvl Lc,
+                                                      BcSpec bc) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+    double pv[1 << D];
+    double rp = 0.0;
+#pragma unroll
+    for (int c = (1 << D) - 1; c >= 0; --c) {
+        pv[c] = P[o0 + (long)c * L.cls];
+        rp = (c == (1 << D) - 1) ? pv[c] : ad(rp, pv[c]);
+    }
+    rp = ml(rp, D == 3 ? 0.125 : 0.25);
+    int cc = 0, cb[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        cc |= (bb[a] & 1) << (D - 1 - a);
+        cb[a] = (bb[a] + 1) >> 1;
+    }
+    const double corr = sb(Pc[at<D>(Lc, cc, cb[0], cb[1], cb[2])], rp);
+    const bool bnd = on_boundary<D>(L, bb);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        const long o = o0 + (long)c * L.cls;
+        const double v = ad(pv[c], corr);
+        P[o] = v;
+        if (bnd) write_pads<D, -1>(P, L, bc, c, bb, o, v);
+    }
+}
+
+// residual into R (edge fields: input of the tangential restriction)
+template <int D, int EA>
+__global__ void __launch_bounds__(256) k_residual_fast(const double* __restrict__ P,
+                                                       const double* __restrict__ F,
+                                                       double* __restrict__ R, Lvl L) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (is_wall<D, EA>(L, c, bb)) continue;
+        const long o = o0 + (long)c * L.cls;
+        R[o] = sb(F[o], op_fast<D>(P, L, c, o));
+    }
+}
+
+// outer residual sum of squares: per-CTA fixed-order partials
+template <int D, int EA>
+__global__ void __launch_bounds__(256) k_res_sumsq_fast(const double* __restrict__ P,
+                                                        const double* __restrict__ F, Lvl L,
+                                                        double* __restrict__ part) {
+    int bb[3];
+    double acc = 0.0;
+    if (tile_coords<D>(L, bb)) {
+        const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+#pragma unroll
+        for (int c = 0; c < (1 << D); ++c) {
+            if (is_wall<D, EA>(L, c, bb)) continue;
+            const long o = o0 + (long)c * L.cls;
+            const double r = sb(F[o], op_fast<D>(P, L, c, o));
+            acc = ad(acc, ml(r, r));
+        }
+    }
+    // fixed-order tree over the CTA (block sizes are powers of two <= 256)
+    __shared__ double red[256];
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nt = blockDim.x * blockDim.y * blockDim.z;
+    red[tid] = acc;
+    __syncthreads();
+    for (int s = nt >> 1; s > 0; s >>= 1) {
+        if (tid < s) red[tid] = ad(red[tid], red[tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0) part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = red[0];
+}
+
