@@ -118,6 +118,20 @@ long fasmg_view_sum_chunks(int dim, const int* ext);
 int fasmg_sub_mean(double* v, const long* vs, int dim, const int* ext, const double* total,
                    double count, void* stream);
 
+/* staggered operators (PKG/stencil.py:114-156): gradient_axis into a
+ * contiguous edge-interior array; divergence of component core views into a
+ * cell interior view */
+int fasmg_gradient_axis(const double* pcore, const long* ps, double* out, int dim,
+                        const int* n, int axis, double inv_h, void* stream);
+int fasmg_divergence(const double* const* comps, const long* cs, double* out, const long* os,
+                     int dim, const int* n, double inv_h, void* stream);
+/* projection-step elementwise ops (ns.py; op codes in fasmg_natural.cu NsOp)
+ * and the 5/7-point Laplacian at a field's interior points */
+int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
+                  const long* is, double s0, double s1, int dim, const int* ext, void* stream);
+int fasmg_laplacian(double* out, const long* os, const double* pcore, const long* ps, int dim,
+                    const int* m, double inv_h2, void* stream);
+
 /* ---- (b2) solver engine: FasSolver (PKG/fas.py:63-162) ------------------ */
 /* FasSolver.__init__ (PKG/fas.py:71-89): n[dim] finest cells, mesh_level
  * coarsenings, operator a*p - b*Lap(p) (PKG/stencil.py:21-38), smoothing
@@ -141,7 +155,7 @@ int fasmg_engine_store(void* engine, double* pcore, const long* ps);
  * CUDA graph */
 int fasmg_engine_run(void* engine, int count, int with_norm, double* sumsq, int use_graph);
 int fasmg_engine_residual_sumsq(void* engine, double* sumsq);
-long fasmg_engine_kernels_per_vcycle(void* engine);
+long fasmg_engine_kernels_per_vcycle(void* engine, int with_norm);
 /* mean duration (ms, CUDA events on the engine stream) of one smoothing
  * half-sweep launch on `level`, over `reps` launches */
 int fasmg_engine_time_sweeps(void* engine, int level, int reps, double* ms);

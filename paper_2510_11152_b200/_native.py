@@ -99,7 +99,7 @@ def lib():
         L.fasmg_engine_create.restype = _vp
         L.fasmg_engine_destroy.argtypes = [_vp]
         L.fasmg_engine_destroy.restype = None
-        L.fasmg_engine_kernels_per_vcycle.argtypes = [_vp]
+        L.fasmg_engine_kernels_per_vcycle.argtypes = [_vp, ctypes.c_int]
         L.fasmg_engine_kernels_per_vcycle.restype = ctypes.c_long
         _lib = L
     return _lib

@@ -399,6 +399,7 @@ struct Engine {
     cudaGraph_t graph_v = nullptr, graph_vn = nullptr;
     cudaGraphExec_t exec_v = nullptr, exec_vn = nullptr;
     long kernels_per_vcycle = 0;
+    long kernels_per_vcycle_norm = 0;
     int sweep_variant = 0;  // 0: thread per block, 1: per (block, class), 2: 2.5D march
     int march_chunk = 32;   // planes per marching chunk
 };
@@ -618,7 +619,8 @@ static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* e
     if (e != cudaSuccess) return fasmg_check(e);
     e = cudaGraphInstantiate(ex, *g, 0);
     if (e != cudaSuccess) return fasmg_check(e);
-    if (!with_norm) E.kernels_per_vcycle = cnt;
+    if (with_norm) E.kernels_per_vcycle_norm = cnt;
+    else E.kernels_per_vcycle = cnt;
     return 0;
 }
 
@@ -867,7 +869,12 @@ int fasmg_engine_time_sweeps(void* h, int k, int reps, double* ms) {
     return st ? st : fasmg_check_launch();
 }
 
-long fasmg_engine_kernels_per_vcycle(void* h) { return ((Engine*)h)->kernels_per_vcycle; }
+// kernels launched per V-cycle (with_norm: V-cycle + outer residual norm),
+// counted while building the graph; 0 before the first captured run
+long fasmg_engine_kernels_per_vcycle(void* h, int with_norm) {
+    Engine* E = (Engine*)h;
+    return with_norm ? E->kernels_per_vcycle_norm : E->kernels_per_vcycle;
+}
 
 // Device pointer and geometry of a level's blocked arrays (tests/bench).
 int fasmg_engine_level_info(void* h, int k, long* info) {

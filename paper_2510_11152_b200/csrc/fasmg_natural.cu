@@ -509,6 +509,85 @@ __global__ void k_div(Comps C, double* out, S3 os, int dim, int n0, int n1, int 
     out[I3(os.s, x[0] - 1, x[1] - 1, x[2] - (dim == 3 ? 1 : 0))] = acc;
 }
 
+// ------------------------------------------------ projection-step elementwise
+// Interior-shaped elementwise ops of the NS drivers (ns.py).  The reference
+// has no NS driver; the association order of
+// each op is fixed here and mirrored by the oracle composition
+// (oracle/ns_oracle.py).
+enum NsOp : int {
+    NS_MIX_EXT = 0,  // (3a - b) * 0.5         (3u^n - u^{n-1})/2
+    NS_MIX_AVG = 1,  // (a + b) * 0.5          (u^n + u~)/2
+    NS_AVG4 = 2,     // 0.25 * ((a + b) + (c + d))   PKG/weno.py:51
+    NS_AXPY = 3,     // a - s0 * b             u = u~ - dt * grad p~
+    NS_ADD = 4,      // a + b                  p = p^n + p~
+    NS_COPY = 5,     // a
+    NS_RHS1 = 6,     // (a - s0*b) - s0*c      u^n - dt*conv - dt*grad p^n
+    NS_RHS2 = 7,     // ((a - s0*b) - s0*c) + s1*d    ... + dt/(2Re) Lap u^n
+    NS_NEG = 8,      // -a                     -div u~
+};
+
+struct V4 { const double* p[4]; S3 s[4]; };
+
+__global__ void k_ns_elem(int op, double* out, S3 os, V4 in, double s0, double s1, int dim,
+                          int e0, int e1, int e2) {
+    long n = (long)e0 * e1 * (dim == 3 ? e2 : 1);
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int x[3];
+    if (dim == 3) {
+        x[2] = (int)(t % e2);
+        long r = t / e2;
+        x[1] = (int)(r % e1);
+        x[0] = (int)(r / e1);
+    } else {
+        x[1] = (int)(t % e1);
+        x[0] = (int)(t / e1);
+        x[2] = 0;
+    }
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        v[k] = in.p[k] ? in.p[k][I3(in.s[k].s, x[0], x[1], x[2])] : 0.0;
+    double r;
+    switch (op) {
+        case NS_MIX_EXT: r = ml(sb(ml(3.0, v[0]), v[1]), 0.5); break;
+        case NS_MIX_AVG: r = ml(ad(v[0], v[1]), 0.5); break;
+        case NS_AVG4: r = ml(0.25, ad(ad(v[0], v[1]), ad(v[2], v[3]))); break;
+        case NS_AXPY: r = sb(v[0], ml(s0, v[1])); break;
+        case NS_ADD: r = ad(v[0], v[1]); break;
+        case NS_COPY: r = v[0]; break;
+        case NS_RHS1: r = sb(sb(v[0], ml(s0, v[1])), ml(s0, v[2])); break;
+        case NS_RHS2: r = ad(sb(sb(v[0], ml(s0, v[1])), ml(s0, v[2])), ml(s1, v[3])); break;
+        default: r = -v[0]; break;
+    }
+    out[I3(os.s, x[0], x[1], x[2])] = r;
+}
+
+// 5/7-point Laplacian (nsum - 2d*c) * inv_h2 (KER/numpy_backend.py:66-88)
+__global__ void k_lap(double* out, S3 os, const double* p, S3 ps, int dim, int m0, int m1,
+                      int m2, double inv_h2) {
+    long n = (long)m0 * m1 * (dim == 3 ? m2 : 1);
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int x[3];
+    if (dim == 3) {
+        x[2] = 1 + (int)(t % m2);
+        long r = t / m2;
+        x[1] = 1 + (int)(r % m1);
+        x[0] = 1 + (int)(r / m1);
+    } else {
+        x[1] = 1 + (int)(t % m1);
+        x[0] = 1 + (int)(t / m1);
+        x[2] = 0;
+    }
+    long o = I3(ps.s, x[0], x[1], x[2]);
+    double c = p[o];
+    double ns = ad(ad(ad(p[o + ps.s[0]], p[o - ps.s[0]]), p[o + ps.s[1]]), p[o - ps.s[1]]);
+    if (dim == 3) ns = ad(ad(ns, p[o + ps.s[2]]), p[o - ps.s[2]]);
+    out[I3(os.s, x[0] - 1, x[1] - 1, x[2] - (dim == 3 ? 1 : 0))] =
+        ml(sb(ns, ml(dim == 3 ? 6.0 : 4.0, c)), inv_h2);
+}
+
 }  // namespace fasmg
 
 // ===========================================================================
@@ -788,6 +867,34 @@ int fasmg_divergence(const double* const* comps, const long* cs, double* out, co
     long tot = (long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
     LAUNCH(tot, (k_div<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(C, out, o, dim, n[0], n[1],
                                                               dim == 3 ? n[2] : 1, inv_h)));
+}
+
+// generic interior elementwise op (NsOp); views: out + up to 4 inputs
+// (NULL allowed), all with element strides [3], extents ext[dim]
+int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
+                  const long* is, double s0, double s1, int dim, const int* ext, void* stream) {
+    V4 v;
+    for (int k = 0; k < 4; ++k) {
+        v.p[k] = in[k];
+        for (int b = 0; b < 3; ++b) v.s[k].s[b] = is[3 * k + b];
+        if (dim == 2) v.s[k].s[2] = 0;
+    }
+    S3 o = mk(os);
+    if (dim == 2) o.s[2] = 0;
+    long tot = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
+    LAUNCH(tot, (k_ns_elem<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(op, out, o, v, s0, s1, dim,
+                                                                  ext[0], ext[1],
+                                                                  dim == 3 ? ext[2] : 1)));
+}
+
+// Laplacian of a field at its interior points: p core view, out interior-shaped
+int fasmg_laplacian(double* out, const long* os, const double* pcore, const long* ps, int dim,
+                    const int* m, double inv_h2, void* stream) {
+    S3 o = mk(os), pp = mk(ps);
+    if (dim == 2) { o.s[2] = 0; pp.s[2] = 0; }
+    long tot = (long)m[0] * m[1] * (dim == 3 ? m[2] : 1);
+    LAUNCH(tot, (k_lap<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(out, o, pcore, pp, dim, m[0], m[1],
+                                                              dim == 3 ? m[2] : 1, inv_h2)));
 }
 
 }  // extern "C"

@@ -1,0 +1,48 @@
+"""Interior elementwise kernels of the projection drivers (fasmg_ns_elem,
+fasmg_laplacian in csrc/fasmg_natural.cu).  Each call is one native launch
+on torch's current stream; views may have any strides."""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+
+MIX_EXT, MIX_AVG, AVG4, AXPY, ADD, COPY, RHS1, RHS2, NEG = range(9)
+
+
+def elem(op: int, out: torch.Tensor, inputs, s0: float = 0.0, s1: float = 0.0) -> torch.Tensor:
+    ins = list(inputs) + [None] * (4 - len(inputs))
+    for t in ins:
+        if t is not None and tuple(t.shape) != tuple(out.shape):
+            raise ValueError(f"shape mismatch {tuple(t.shape)} vs {tuple(out.shape)}")
+    ptrs = (ctypes.c_void_p * 4)(*[(t.data_ptr() if t is not None else None) for t in ins])
+    st = []
+    for t in ins:
+        s = list(t.stride()) if t is not None else []
+        st += s + [0] * (3 - len(s))
+    L = N.lib()
+    L.fasmg_ns_elem.restype = ctypes.c_int
+    N.require_cuda(out)
+    N.check(L.fasmg_ns_elem(ctypes.c_int(op), N.ptr(out), N.strides(out), ptrs,
+                            (ctypes.c_long * 12)(*st), ctypes.c_double(s0), ctypes.c_double(s1),
+                            ctypes.c_int(out.dim()), N.ints(out.shape), N.torch_stream()))
+    return out
+
+
+def laplacian(field, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(nsum - 2d*c) / h^2 at the interior points of a field with fresh ghosts
+    (the _lap helper of KER/numpy_backend.py:66-88)."""
+    shape = field.interior_shape
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float64, device=field.device)
+    pc = field.core
+    L = N.lib()
+    L.fasmg_laplacian.restype = ctypes.c_int
+    N.check(L.fasmg_laplacian(N.ptr(out), N.strides(out), N.ptr(pc), N.strides(pc),
+                              ctypes.c_int(field.grid.dim), N.ints(shape),
+                              ctypes.c_double(1.0 / (field.grid.h * field.grid.h)),
+                              N.torch_stream()))
+    return out

@@ -107,8 +107,16 @@ class _Engine:
                ctypes.byref(out), 1 if use_graph else 0)
         return out.value
 
-    def kernels_per_vcycle(self) -> int:
-        return int(N.lib().fasmg_engine_kernels_per_vcycle(self.handle))
+    def kernels_per_vcycle(self, with_norm: bool = True) -> int:
+        """Kernels launched by one captured V-cycle (+ norm) graph."""
+        return int(N.lib().fasmg_engine_kernels_per_vcycle(self.handle, 1 if with_norm else 0))
+
+    def time_sweeps(self, level: int = 0, reps: int = 20) -> float:
+        """Mean duration (ms) of one smoothing half-sweep launch on `level`,
+        CUDA events on the engine stream."""
+        ms = ctypes.c_double()
+        N.call("fasmg_engine_time_sweeps", self.handle, int(level), int(reps), ctypes.byref(ms))
+        return ms.value
 
 
 class FasSolver:

@@ -1,0 +1,64 @@
+"""Projection steppers on the GPU vs the composed CPU oracle
+(oracle/ns_oracle.py), and classical vs memory-efficient schedules."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_11152_b200 as pkg
+    return pkg
+
+
+def _stepper(P, n, order, mode, dt=1e-2, re=100.0):
+    from paper_2510_11152_b200.ns import NSParams, ProjectionStepper, cavity_bcs
+    g = P.unit_grid(n)
+    st = ProjectionStepper(g, NSParams(re=re, dt=dt, order=order, mode=mode, tol=1e-10, k_max=20))
+    st.set_state({})
+    return st
+
+
+@pytest.mark.parametrize("n,order", [((16, 16), 1), ((16, 16), 2), ((8, 8, 8), 1), ((8, 8, 8), 2)])
+def test_ns_matches_oracle(P, n, order):
+    import ns_oracle as NO
+    st = _stepper(P, n, order, "efficient")
+    orc = NO.NSOracle(n, 100.0, 1e-2, order)
+    for k in range(3):
+        rep = st.step()
+        hist = orc.step()
+        for c in st.comps:
+            np.testing.assert_allclose(rep.momentum[c].residual_history, hist[c], rtol=1e-10)
+        np.testing.assert_allclose(rep.pressure.residual_history, hist["p"], rtol=1e-10)
+        for c in st.comps:
+            got = st.velocity(c).numpy()
+            assert np.array_equal(got.view(np.uint64), orc.un[c].data.view(np.uint64)), (k, c)
+        gp = st.pressure().interior.cpu().numpy()
+        assert np.array_equal(gp, orc.p.interior), k
+
+
+@pytest.mark.parametrize("dim,order", [(2, 1), (2, 2), (3, 1), (3, 2)])
+def test_classical_equals_efficient(P, dim, order):
+    n = (16,) * dim if dim == 2 else (8,) * 3
+    a = _stepper(P, n, order, "efficient")
+    b = _stepper(P, n, order, "classical")
+    assert a.resident_count() == 2 * dim + 2
+    assert b.resident_count() == (3 if order == 1 else 4) * dim + 3
+    for _ in range(3):
+        a.step()
+        b.step()
+    for c in a.comps:
+        assert torch.equal(a.velocity(c).interior, b.velocity(c).interior)
+    assert torch.equal(a.pressure().interior, b.pressure().interior)
+
+
+def test_divergence_free_after_projection(P):
+    st = _stepper(P, (32, 32), 2, "efficient")
+    for _ in range(5):
+        st.step()
+        assert abs(st.divergence()) <= 1e-12
