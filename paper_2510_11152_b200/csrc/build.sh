@@ -12,7 +12,12 @@ OBJS=()
 mkdir -p "${HERE}/../build"
 for src in fasmg_runtime fasmg_natural fasmg_engine; do
   obj="${HERE}/../build/${src}.o"
-  if [[ ! -f "$obj" || "${HERE}/${src}.cu" -nt "$obj" || "${HERE}/fasmg_common.cuh" -nt "$obj" || "${HERE}/fasmg_internal.h" -nt "$obj" ]]; then
+  stale=0
+  [[ -f "$obj" ]] || stale=1
+  for dep in "${HERE}/${src}.cu" "${HERE}"/*.cuh "${HERE}"/*.h "${HERE}/build.sh"; do
+    [[ "$dep" -nt "$obj" ]] && stale=1
+  done
+  if [[ $stale == 1 ]]; then
     "$NVCC" "${FLAGS[@]}" -c "${HERE}/${src}.cu" -o "$obj" &
   fi
   OBJS+=("$obj")

@@ -400,8 +400,11 @@ struct Engine {
     cudaGraphExec_t exec_v = nullptr, exec_vn = nullptr;
     long kernels_per_vcycle = 0;
     long kernels_per_vcycle_norm = 0;
-    int sweep_variant = 0;  // 0: thread per block, 1: per (block, class), 2: 2.5D march
-    int march_chunk = 32;   // planes per marching chunk
+    // 0: thread per block, 1: per (block, class), 2: 2.5D register march,
+    // 3: 2.5D shared-memory march for large 3D levels (default), else 0
+    int sweep_variant = 3;
+    int march_chunk = 0;    // planes per marching chunk (0: per-level default)
+    int sweep_minb = 3;     // min resident CTAs of the 3D half-sweep (register cap)
 };
 
 struct Tile {
@@ -465,7 +468,7 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         return;
     }
     if (E.sweep_variant == 2 && __builtin_popcount(M) > 1) {
-        const int chunk = E.march_chunk;
+        const int chunk = E.march_chunk > 0 ? E.march_chunk : 16;
         dim3 blk, grd;
         const unsigned nch = (L.B[0] + chunk - 1) / chunk;
         if (D == 3) {
@@ -481,7 +484,23 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         k_sweep_march<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
         return;
     }
-    k_sweep_fast<D, EA, M><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
+    if (D == 3 && E.sweep_variant == 3 && __builtin_popcount(M) > 1 && L.B[2] >= 32 &&
+        L.B[1] >= 8 && L.B[0] >= 128) {
+        using namespace smem_sweep;
+        // planes per marching chunk: long chunks amortize the two window
+        // planes each chunk loads twice; short ones keep enough CTAs
+        // (measured on B200: 16 at B0 >= 256, 4 at B0 = 128)
+        const int chunk = E.march_chunk > 0 ? E.march_chunk : (L.B[0] >= 256 ? 16 : 4);
+        dim3 blk(TX, TY, 1);
+        dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
+        const size_t shm = sizeof(double) * 4 * RING * PL;
+        k_sweep_smem<EA, M><<<grd, blk, shm, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
+        return;
+    }
+    if (D == 3 && E.sweep_minb == 4 && __builtin_popcount(M) > 1)
+        k_sweep_fast<D, EA, M, 4><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
+    else
+        k_sweep_fast<D, EA, M><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
 }
 
 template <int D, int EA>
@@ -703,8 +722,9 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
         }
     E->masks.assign(masks, masks + nmasks);
     if (const char* v = getenv("FASMG_SWEEP_VARIANT")) E->sweep_variant = atoi(v);
-    if (const char* v = getenv("FASMG_MARCH_CHUNK")) E->march_chunk = std::max(1, atoi(v));
+    if (const char* v = getenv("FASMG_MARCH_CHUNK")) E->march_chunk = std::max(0, atoi(v));
     if (const char* v = getenv("FASMG_TILE_Y")) g_tile_y = std::max(1, atoi(v));
+    if (const char* v = getenv("FASMG_SWEEP_MINB")) E->sweep_minb = atoi(v);
     int nn[3] = {n[0], n[1], dim == 3 ? n[2] : 2};
     for (int k = 0; k < E->nl; ++k) {
         E->L[k] = make_lvl(dim, nn, ea, dmin, dmax, a, b);

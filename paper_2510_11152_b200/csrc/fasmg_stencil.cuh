@@ -160,8 +160,8 @@ __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
 // ------------------------------------------------------------- smoothing
 // One launch = the reference's colors whose classes are in MASK (mutually
 // independent classes; PKG/smoothers.py:136-153).  Thread per block.
-template <int D, int EA, unsigned MASK>
-__global__ void __launch_bounds__(256) k_sweep_fast(double* __restrict__ P,
+template <int D, int EA, unsigned MASK, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) k_sweep_fast(double* __restrict__ P,
                                                     const double* __restrict__ F, Lvl L,
                                                     BcSpec bc) {
     int bb[3];
@@ -380,6 +380,150 @@ __global__ void __launch_bounds__(256) k_sweep_march(double* __restrict__ P,
                 w0[k] = w1[k];
                 w1[k] = wn[k];
             }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if ((MASK >> c) & 1u) fv[c] = fn[c];
+        }
+    }
+}
+
+// 2.5D marching half-sweep staged through shared memory (3D, large levels).
+// A CTA owns a 32 (b2) x 8 (b1) tile of block columns and marches a chunk
+// of planes along b0.  For each opposite-parity class it keeps a ring of 3
+// plane tiles (with a 1-block in-plane halo) in shared memory: two planes
+// are the class's current axis-0 window, the third is being filled by
+// cp.async for the next step, so DRAM loads stay in flight independently of
+// registers.  f is prefetched one plane ahead in registers.  Arithmetic and
+// pad maintenance are those of k_sweep_fast.
+namespace smem_sweep {
+constexpr int TX = 32, TY = 8, RX = TX + 2, RY = TY + 2, PL = RX * RY, RING = 3;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int EA, unsigned MASK>
+__global__ void __launch_bounds__(256) k_sweep_smem(double* __restrict__ P,
+                                                    const double* __restrict__ F, Lvl L,
+                                                    BcSpec bc, int chunk) {
+    using namespace smem_sweep;
+    constexpr int D = 3, NC = 8;
+    constexpr unsigned OPP = opp_mask<3>(MASK);
+    extern __shared__ double sm[];  // [4 opp classes][RING][PL]
+    // opposite class -> ring index (compile time)
+    auto ridx = [](int k) {
+        int n = 0;
+        for (int t = 0; t < k; ++t) n += (OPP >> t) & 1u;
+        return n;
+    };
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int x0 = blockIdx.x * TX + 1, y0 = blockIdx.y * TY + 1;
+    const int b0s = 1 + blockIdx.z * chunk;
+    const int b0e = min(L.B[0], b0s + chunk - 1);
+    int bb[3];
+    bb[2] = x0 + tx;
+    bb[1] = y0 + ty;
+    const bool active = bb[1] <= L.B[1] && bb[2] <= L.B[2];
+    const long s0 = L.s0, s1 = L.s1;
+
+    auto load_plane = [&](int k, int pb) {
+        double* dst = sm + (ridx(k) * RING + (pb % RING)) * PL;
+        const double* src = P + (long)k * L.cls + (long)pb * s0 + OFF;
+        for (int e = tid; e < PL; e += TX * TY) {
+            const int r = e / RX, cx = e - r * RX;
+            const int gb1 = min(y0 - 1 + r, L.B[1] + 1);
+            const int gb2 = min(x0 - 1 + cx, L.B[2] + 1);
+            cp_async8(dst + e, src + (long)gb1 * s1 + gb2);
+        }
+    };
+    // prologue: both window planes of every opposite class
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        if (!((OPP >> k) & 1u)) continue;
+        const int lo = (k & 4) ? b0s : b0s - 1;
+        load_plane(k, lo);
+        load_plane(k, lo + 1);
+    }
+    cp_async_commit();
+    const long col = active ? at<D>(L, 0, 0, bb[1], bb[2]) : 0;
+    double fv[NC], fn[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if ((MASK >> c) & 1u) fv[c] = active ? __ldg(F + col + (long)c * L.cls + (long)b0s * s0) : 0.0;
+
+    for (int b0 = b0s; b0 <= b0e; ++b0) {
+        const bool more = b0 < b0e;
+        if (more) {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                if (!((OPP >> k) & 1u)) continue;
+                const int lo = (k & 4) ? b0 : b0 - 1;
+                load_plane(k, lo + 2);
+            }
+            cp_async_commit();
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if ((MASK >> c) & 1u)
+                    fn[c] = active ? __ldg(F + col + (long)c * L.cls + (long)(b0 + 1) * s0) : 0.0;
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (active) {
+            bb[0] = b0;
+            const long pl = col + (long)b0 * s0;
+            const int ci = (ty + 1) * RX + (tx + 1);
+            double nv[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                if (!((MASK >> c) & 1u)) continue;
+                // axis 0: window (lo, lo+1) of class c^4 -> E = lo+1, W = lo
+                const int k0 = c ^ 4;
+                const int lo0 = (k0 & 4) ? b0 : b0 - 1;
+                const double* w0 = sm + ridx(k0) * RING * PL;
+                double ns = ad(w0[((lo0 + 1) % RING) * PL + ci], w0[(lo0 % RING) * PL + ci]);
+                // axis 1 (b1 = rows), class c^2 at plane b0
+                {
+                    const int k1 = c ^ 2;
+                    const double* w = sm + (ridx(k1) * RING + (b0 % RING)) * PL;
+                    const bool q = (c & 2) != 0;
+                    const double e = w[ci + (q ? 0 : RX)];
+                    const double wv = w[ci - (q ? RX : 0)];
+                    ns = ad(ad(ns, e), wv);
+                }
+                // axis 2 (b2 = cols), class c^1 at plane b0
+                {
+                    const int k2 = c ^ 1;
+                    const double* w = sm + (ridx(k2) * RING + (b0 % RING)) * PL;
+                    const bool q = (c & 1) != 0;
+                    const double e = w[ci + (q ? 0 : 1)];
+                    const double wv = w[ci - (q ? 1 : 0)];
+                    ns = ad(ad(ns, e), wv);
+                }
+                nv[c] = ad(ml(L.h2, fv[c]), ml(L.b, ns));
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+            const bool bnd = bb[0] == 1 || bb[0] == L.B[0] || bb[1] == 1 || bb[1] == L.B[1] ||
+                             bb[2] == 1 || bb[2] == L.B[2];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                if (!((MASK >> c) & 1u)) continue;
+                if (is_wall<D, EA>(L, c, bb)) continue;
+                const long o = pl + (long)c * L.cls;
+                P[o] = nv[c];
+                if (bnd) write_pads<D, EA>(P, L, bc, c, bb, o, nv[c]);
+            }
+        }
+        __syncthreads();  // the next prefetch overwrites the oldest ring slot
+        if (more) {
 #pragma unroll
             for (int c = 0; c < NC; ++c)
                 if ((MASK >> c) & 1u) fv[c] = fn[c];
