@@ -1,7 +1,7 @@
 """Benchmark: MDOF/s per FAS V-cycle, 3D heat 512^3, % of HBM roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--n 512] [--dim 3] [--no-cpu-baseline]
+                    [--grid 512] [--dim 3] [--no-cpu-baseline]
 
 Workload (BASELINE.json configs[2], the config the metric is quoted on):
 one backward-Euler heat step p - dt*Lap(p) = f with dt = 1 (a = b = 1) on a
@@ -32,9 +32,12 @@ test -- the paper's per-"iteration" time.
 * --impl reference: the same metric from the oracle port alone (the
   reference is pure Python+numba and does not travel to the GPU box).
 
-Multi-GPU (torchrun, one process per GPU): ranks run independent replicas
-of the workload (the axis-0 slab decomposition is not wired into bench.py
-yet); value = all DOF processed / max-over-ranks time.
+Multi-GPU (torchrun, one process per GPU): the SAME 512^3 problem is split
+into axis-0 slabs (paper_2510_11152_b200/slab.py DistSlabSolver): halo
+planes are pushed into the neighbours' memory after every smoothing
+half-sweep over CUDA IPC / NVLink, coarse levels are all-gathered and
+solved redundantly, the residual is reduced in rank order.  Strong
+scaling: value = 512^3 / max-over-ranks time per step.
 """
 
 from __future__ import annotations
@@ -63,7 +66,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--grid", dest="n", type=int, default=512)
     ap.add_argument("--dim", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -244,28 +247,65 @@ def b200_arm(args):
     rank, world, local = dist_env()
     if world != args.gpus and rank == 0:
         print(f"[bench] warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    shared = world > ndev  # functional test: several ranks on one device
+    dev = torch.device("cuda", local % ndev)
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     n, dim = args.n, args.dim
     K, W = args.steps, max(args.warmup, 3)
     g, p0, shape, inner = make_inputs(n, dim)
     from paper_2510_11152_b200 import manufactured as M
     f_dev = M.poisson_rhs_discrete(g, device=dev)  # f = L_h(p_exact) on the device
-    f_host_int = f_dev.interior.cpu().numpy()
-    p = Field(g, Location.CELL, 1, p0, device=dev)
-    f = Field(g, Location.CELL, 1, f_dev.data.clone())
     coeffs = P.OperatorCoeffs(1.0, 1.0)
     ml = int(np.log2(n)) - 1
     plan = P.make_plan("x", dim, "ff")
     bc = P.BoundaryCondition.dirichlet(dim)
-    solver = P.FasSolver(P.make_hierarchy(g, ml), Location.CELL, bc, plan, coeffs)
-    eng = solver.engine(2, dev)
-    eng.load(p, f)
+    hier = P.make_hierarchy(g, ml)
+    dof = n ** dim
+
+    if world == 1:
+        p = Field(g, Location.CELL, 1, p0, device=dev)
+        f = Field(g, Location.CELL, 1, f_dev.data.clone())
+        solver = P.FasSolver(hier, Location.CELL, bc, plan, coeffs)
+        eng = solver.engine(2, dev)
+        eng.load(p, f)
+        run_step = lambda: eng.run(1, with_norm=True)  # noqa: E731
+        stream_handle = eng.stream.value
+        local_dof = dof
+        parallelism = "single"
+    else:
+        from paper_2510_11152_b200.slab import DistSlabSolver, slab_view
+        ds = DistSlabSolver(hier, Location.CELL, bc, plan, coeffs, 2, dev)
+        pg = torch.from_numpy(p0).to(dev)
+        fg = f_dev.data.clone()
+        pv = slab_view(pg, 1, n, world, rank)
+        fv = slab_view(fg, 1, n, world, rank)
+        ds.load(pv, fv)
+        eng = ds.engine
+
+        def run_step():
+            eng.launch(1, True)
+            return eng.result()
+        stream_handle = eng.stream.value
+        local_dof = dof // world
+        parallelism = (f"z-slab x{world} (axis-0 slabs, halo push per half-sweep over "
+                       f"CUDA IPC/NVLink, coarse levels >= {eng.kg} gathered)"
+                       + (" [ranks sharing one device: functional test only]" if shared else ""))
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -275,8 +315,8 @@ def b200_arm(args):
     # --- device-resident timed region: K outer iterations (V-cycle + norm,
     #     host reads the residual each step exactly as FasSolver.solve does)
     for _ in range(W):
-        eng.run(1, with_norm=True)
-    st = torch.cuda.ExternalStream(eng.stream.value, device=dev)
+        run_step()
+    st = torch.cuda.ExternalStream(stream_handle, device=dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if dist is not None:
@@ -286,23 +326,19 @@ def b200_arm(args):
     ev0.record(st)
     hist = []
     for _ in range(K):
-        hist.append(eng.run(1, with_norm=True))
+        hist.append(run_step())
     ev1.record(st)
     torch.cuda.synchronize()
     t1 = time.time()
     clocks.mark(t0, t1)
-    ms_step = ev0.elapsed_time(ev1) / K
+    ms_step = max_over_ranks(ev0.elapsed_time(ev1) / K)
     if dist is not None:
-        tt = torch.tensor([ms_step], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_step = float(tt.item())
         dist.barrier()
-    dof = n ** dim
-    value = world * dof / (ms_step * 1e-3) / 1e6
+    value = dof / (ms_step * 1e-3) / 1e6
 
     # --- live per-launch timing of the dominant kernel (finest half-sweep)
     sweep_ms = eng.time_sweeps(0, 16)
-    achieved = BYTES_PER_DOF_HALF_SWEEP * dof / (sweep_ms * 1e-3) / 1e9
+    achieved = BYTES_PER_DOF_HALF_SWEEP * local_dof / (sweep_ms * 1e-3) / 1e9
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(peaks_path):
@@ -313,7 +349,7 @@ def b200_arm(args):
             pass
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         try:
             d = json.load(open(prof))
             if d.get("n") == n and d.get("dim") == dim:
@@ -322,36 +358,59 @@ def b200_arm(args):
             pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": ("k_sweep_smem" if dim == 3 else "k_sweep_fast") + " (finest-level X-MCGS half-sweep)",
+                "kernel": ("k_sweep_smem" if dim == 3 else "k_sweep_fast")
+                          + " (finest-level X-MCGS half-sweep)",
                 "kernel_ms": sweep_ms,
-                "algorithmic_bytes_per_launch": BYTES_PER_DOF_HALF_SWEEP * dof,
+                "algorithmic_bytes_per_launch": BYTES_PER_DOF_HALF_SWEEP * local_dof,
                 "peak_source": peak_src,
-                "vcycle_model_GBps": (259.4 if dim == 3 else 306.7) * dof / (ms_step * 1e-3) / 1e9}
+                "vcycle_model_GBps_per_gpu": (259.4 if dim == 3 else 306.7) * local_dof
+                                             / (ms_step * 1e-3) / 1e9}
 
-    kernels = eng.kernels_per_vcycle(True)
+    from paper_2510_11152_b200 import _native as N
+    kernels = int(N.lib().fasmg_engine_kernels_per_vcycle(eng.handle, 1))
 
-    # --- e2e through the public API with host buffers
+    # --- e2e through the public API with host buffers (single GPU: Field +
+    #     solve(kMax=1); slabs: per-rank slab copies + DistSlabSolver)
     e2e_steps = args.e2e_steps or max(3, min(K, 5))
-    ph = torch.from_numpy(p0).pin_memory()
-    fh = torch.empty(shape, dtype=torch.float64).pin_memory()
-    fh.copy_(f_dev.data.cpu())
-    out_h = torch.empty(shape, dtype=torch.float64).pin_memory()
-    pe = Field(g, Location.CELL, 1, device=dev)
-    fe = Field(g, Location.CELL, 1, device=dev)
-    params1 = P.FasParams(1e-9, 1, 2, ml)
     cur = torch.cuda.current_stream(dev)
+    if world == 1:
+        ph = torch.from_numpy(p0).pin_memory()
+        fh = torch.empty(shape, dtype=torch.float64).pin_memory()
+        fh.copy_(f_dev.data.cpu())
+        out_h = torch.empty(shape, dtype=torch.float64).pin_memory()
+        pe = Field(g, Location.CELL, 1, device=dev)
+        fe = Field(g, Location.CELL, 1, device=dev)
+        params1 = P.FasParams(1e-9, 1, 2, ml)
 
-    def e2e_step():
-        pe.data.copy_(ph, non_blocking=True)
-        fe.data.copy_(fh, non_blocking=True)
-        rep = solver.solve(pe, fe, params1)
-        out_h.copy_(pe.data, non_blocking=True)
-        return rep
+        def e2e_step():
+            pe.data.copy_(ph, non_blocking=True)
+            fe.data.copy_(fh, non_blocking=True)
+            solver.solve(pe, fe, params1)
+            out_h.copy_(pe.data, non_blocking=True)
+        h2d = 2 * int(np.prod(shape)) * 8
+        d2h = int(np.prod(shape)) * 8 + 8
+        api = "Field(host pinned -> device) + solve(..., FasParams(k_max=1)) + p -> host"
+    else:
+        ph = pv.cpu().pin_memory()
+        fh = fv.cpu().pin_memory()
+        out_h = torch.empty_like(ph).pin_memory()
 
+        def e2e_step():
+            pv.copy_(ph, non_blocking=True)
+            fv.copy_(fh, non_blocking=True)
+            ds.load(pv, fv)
+            ds.run(1)
+            ds.store(pv)
+            out_h.copy_(pv, non_blocking=True)
+        h2d = 2 * ph.numel() * 8
+        d2h = ph.numel() * 8 + 8
+        api = "rank slab (host pinned -> device) + DistSlabSolver load/run(1)/store + slab -> host"
     e2e_step()  # warm-up
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
     t2 = time.time()
     a.record(cur)
     for _ in range(e2e_steps):
@@ -359,23 +418,17 @@ def b200_arm(args):
     b.record(cur)
     torch.cuda.synchronize()
     clocks.mark(t2, time.time())
-    e2e_ms = a.elapsed_time(b) / e2e_steps
-    if dist is not None:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    e2e = {"value": world * dof / (e2e_ms * 1e-3) / 1e6, "unit": "MDOF/s",
-           "h2d_bytes_per_step": 2 * int(np.prod(shape)) * 8,
-           "d2h_bytes_per_step": int(np.prod(shape)) * 8 + 8,
-           "ms_per_step": e2e_ms, "steps": e2e_steps,
-           "api": "Field(host pinned -> device) + solve(..., FasParams(k_max=1)) + p -> host"}
+    e2e_ms = max_over_ranks(a.elapsed_time(b) / e2e_steps)
+    e2e = {"value": dof / (e2e_ms * 1e-3) / 1e6, "unit": "MDOF/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": e2e_ms, "steps": e2e_steps, "api": api}
     clocks.stop()
 
     # --- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = host_threads()
-        t_cpu = cpu_oracle_vcycle(p0, f_host_int, n, dim, threads)
+        t_cpu = cpu_oracle_vcycle(p0, f_dev.interior.cpu().numpy(), n, dim, threads)
         cpu = {"value": dof / t_cpu / 1e6, "unit": "MDOF/s", "cores": threads, "kind": "port",
                "sample": f"1 V-cycle + residual norm of the same {n}^{dim} inputs on the oracle/ "
                          f"C port of the reference (OpenMP, {threads} threads)",
@@ -384,12 +437,12 @@ def b200_arm(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "MDOF/s", "n_gpus": world, "steps": K,
-            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong",
             "vs_baseline": value / PAPER_4090_MDOFS,
             "vs_baseline_ref": "RTX 4090, 0.4633 s per V-cycle at 3D 512^3 (PAPER.md:510)",
             "dtype": "f64", "data": "synthetic",
-            "config": config_dict(n, dim, "single" if world == 1 else
-                                  f"replicas x{world} (z-slab decomposition not in bench yet)"),
+            "config": config_dict(n, dim, parallelism),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks.summary(), "gpu_launches": kernels * K,
             "kernels_per_step": kernels,
@@ -398,6 +451,8 @@ def b200_arm(args):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
+        if world > 1:
+            ds.close()
         dist.destroy_process_group()
     return 0
 

@@ -161,6 +161,39 @@ long fasmg_engine_kernels_per_vcycle(void* engine, int with_norm);
 int fasmg_engine_time_sweeps(void* engine, int level, int reps, double* ms);
 int fasmg_engine_level_info(void* engine, int level, long* info);
 
+/* ---- axis-0 slab decomposition -------------------
+ * One engine per rank owns the slab `rank` of every level whose block-plane
+ * count splits into >= min_planes (even) planes per rank; coarser levels are
+ * replicated.  After each half-sweep the updated classes' boundary planes
+ * are pushed into the neighbours' halo planes (peer stores over NVLink /
+ * CUDA IPC, or same-device stores for virtual ranks) and published with
+ * system-scope release/acquire counters; the first replicated level is
+ * all-gathered; the residual sum is reduced in fixed rank order.  Cell-
+ * centred fields, x not periodic. */
+void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, double dmax,
+                               int mesh_level, double a, double b, const int* kinds,
+                               const double* vals, int nmasks, const unsigned* masks, int s,
+                               void* stream, int nranks, int rank, int min_planes);
+int fasmg_engine_export_count(void* engine);
+/* device pointers of this engine: P[0..nl), F[0..nl), flags, allpart */
+int fasmg_engine_export(void* engine, unsigned long long* out);
+/* every rank's export arrays, concatenated, as pointers valid in this process */
+int fasmg_engine_connect(void* engine, const unsigned long long* all, int nranks);
+/* [first replicated level, local planes of level 0, global plane offset] */
+int fasmg_engine_slab_info(void* engine, int* out);
+/* push the level-0 halo planes after fasmg_engine_load */
+int fasmg_engine_sync_halos(void* engine);
+/* asynchronous run/result pair (ranks that must run concurrently) */
+int fasmg_engine_launch(void* engine, int count, int with_norm);
+int fasmg_engine_result(void* engine, double* sumsq);
+/* test access: level geometry [cls, s0, s1, E0, E1, E2, B0, off0, G0] and a
+ * device copy of a level's blocked P (which=0) or F (which=1) arrays */
+int fasmg_engine_level_geom(void* engine, int level, long* out);
+int fasmg_engine_level_copy(void* engine, int level, int which, double* dst);
+int fasmg_ipc_get_handle(void* ptr, unsigned char* out64);
+int fasmg_ipc_open_handle(const unsigned char* in64, void** ptr);
+int fasmg_ipc_close_handle(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,13 @@ _SIGS = {
     "fasmg_engine_residual_sumsq": "vD",
     "fasmg_engine_level_info": "viL",
     "fasmg_engine_time_sweeps": "viiD",
+    "fasmg_engine_launch": "vii",
+    "fasmg_engine_level_geom": "viL",
+    "fasmg_engine_level_copy": "viip",
+    "fasmg_engine_result": "vD",
+    "fasmg_engine_sync_halos": "v",
+    "fasmg_engine_slab_info": "vI",
+    "fasmg_ipc_close_handle": "v",
     "fasmg_stream_create": "V",
     "fasmg_stream_destroy": "v",
     "fasmg_stream_synchronize": "v",
@@ -97,6 +104,19 @@ def lib():
             ctypes.c_int, ctypes.c_double, ctypes.c_double, _c_int_p, _c_double_p,
             ctypes.c_int, ctypes.POINTER(ctypes.c_uint), ctypes.c_int, _vp]
         L.fasmg_engine_create.restype = _vp
+        L.fasmg_engine_create_slab.argtypes = L.fasmg_engine_create.argtypes + [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.fasmg_engine_create_slab.restype = _vp
+        L.fasmg_engine_export_count.argtypes = [_vp]
+        L.fasmg_engine_export_count.restype = ctypes.c_int
+        L.fasmg_engine_export.argtypes = [_vp, ctypes.POINTER(ctypes.c_ulonglong)]
+        L.fasmg_engine_export.restype = ctypes.c_int
+        L.fasmg_engine_connect.argtypes = [_vp, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+        L.fasmg_engine_connect.restype = ctypes.c_int
+        L.fasmg_ipc_get_handle.argtypes = [_vp, ctypes.c_char_p]
+        L.fasmg_ipc_get_handle.restype = ctypes.c_int
+        L.fasmg_ipc_open_handle.argtypes = [ctypes.c_char_p, ctypes.POINTER(_vp)]
+        L.fasmg_ipc_open_handle.restype = ctypes.c_int
         L.fasmg_engine_destroy.argtypes = [_vp]
         L.fasmg_engine_destroy.restype = None
         L.fasmg_engine_kernels_per_vcycle.argtypes = [_vp, ctypes.c_int]

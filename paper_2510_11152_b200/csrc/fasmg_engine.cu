@@ -53,7 +53,8 @@ static constexpr int TPB = 256;
 
 struct Lvl {
     int dim, ea;
-    int n[3], B[3], E[3];
+    int n[3], B[3], E[3];  // B[0], E[0]: LOCAL block-plane count (slab) + pads
+    int off0, G0;          // axis-0 global offset of local block 1 (minus 1), global B0
     long s0, s1, cls;  // strides of block axes 0,1 (last axis stride 1)
     long nblk;         // interior blocks
     double h, h2, inv_h2, denom, a, b;
@@ -64,6 +65,9 @@ __device__ __forceinline__ long at(const Lvl& L, int c, int b0, int b1, int b2) 
     if (D == 3) return c * L.cls + b0 * L.s0 + b1 * L.s1 + b2 + OFF;
     return c * L.cls + b0 * L.s0 + b1 + OFF;
 }
+
+template <int D>
+__host__ __device__ __forceinline__ long L_B1(const Lvl& L) { return L.B[1]; }
 
 template <int D>
 __device__ __forceinline__ void decode(const Lvl& L, long t, int* bb) {
@@ -379,6 +383,85 @@ __global__ void k_unpack(const double* __restrict__ src, Lvl L, double* __restri
 
 static inline int nb(long n, int t) { return (int)((n + t - 1) / t); }
 
+// ------------------------------------------------------- slab exchanges
+// Copy the interior (b1, b2) of plane `sp` of the classes in `mask` from a
+// local level array to plane `dp` of a peer's array of the same level
+// geometry (peer memory mapped over NVLink P2P / CUDA IPC, or the same
+// device for virtual ranks), then fence at system scope so a following
+// signal publishes the data.
+template <int D>
+__global__ void k_push_plane(const double* __restrict__ src, double* __restrict__ dst, Lvl Ls,
+                             Lvl Ld, int sp, int dp, unsigned mask) {
+    const long n1 = L_B1<D>(Ls), n2 = D == 3 ? Ls.B[2] : 1;
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (!((mask >> c) & 1u) || t >= n1 * n2) return;
+    const int b1 = 1 + (int)(t / n2), b2 = D == 3 ? 1 + (int)(t % n2) : 0;
+    const double v = src[at<D>(Ls, c, sp, b1, b2)];
+    dst[at<D>(Ld, c, dp, b1, b2)] = v;
+    __threadfence_system();
+}
+
+// Copy planes off+1..off+cnt of every class of a replicated (full) level
+// array into the same planes of a peer's copy (the coarse-level gather).
+template <int D>
+__global__ void k_push_part(const double* __restrict__ src, double* __restrict__ dst, Lvl L,
+                            int off, int cntp) {
+    const long n1 = L.B[1], n2 = D == 3 ? L.B[2] : 1;
+    const long per = n1 * n2;
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (t >= per * cntp) return;
+    const int p = off + 1 + (int)(t / per);
+    const long r = t % per;
+    const int b1 = 1 + (int)(r / n2), b2 = D == 3 ? 1 + (int)(r % n2) : 0;
+    const long o = at<D>(L, c, p, b1, b2);
+    dst[o] = src[o];
+    __threadfence_system();
+}
+
+// single-thread publish: bump my send counter for `peer` and store it into
+// the peer's arrival slot for me (release, system scope)
+__global__ void k_signal(long long* __restrict__ peer_slot, long long* __restrict__ send_cnt) {
+    if (threadIdx.x | blockIdx.x) return;
+    const long long v = *send_cnt + 1;
+    *send_cnt = v;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(peer_slot), "l"(v) : "memory");
+}
+
+// single-thread wait until the arrival counter from a peer reaches the next
+// expected value (acquire, system scope)
+__global__ void k_wait(const long long* __restrict__ my_slot, long long* __restrict__ expect) {
+    if (threadIdx.x | blockIdx.x) return;
+    const long long e = *expect + 1;
+    *expect = e;
+    long long v;
+    const long long t0 = clock64();
+    do {
+        asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(my_slot) : "memory");
+        // a peer that never arrives is a protocol bug: fail loudly (~30 s)
+        // instead of hanging the device
+        if (clock64() - t0 > 60000000000LL) asm volatile("trap;");
+    } while (v < e);
+    __threadfence_system();
+}
+
+// residual partial of this rank (dsum) -> every rank's allpart[rank]
+__global__ void k_put_partial(const double* __restrict__ dsum, double* __restrict__ dst) {
+    if (threadIdx.x | blockIdx.x) return;
+    *dst = *dsum;
+    __threadfence_system();
+}
+
+// fixed rank-order sum of the partials (identical on every rank)
+__global__ void k_sum_partials(const double* __restrict__ allpart, int n, double* out) {
+    if (threadIdx.x | blockIdx.x) return;
+    double s = allpart[0];
+    for (int r = 1; r < n; ++r) s = ad(s, allpart[r]);
+    *out = s;
+}
+
 // ===========================================================================
 // Host engine
 // ===========================================================================
@@ -405,6 +488,20 @@ struct Engine {
     int sweep_variant = 3;
     int march_chunk = 0;    // planes per marching chunk (0: per-level default)
     int sweep_minb = 3;     // min resident CTAs of the 3D half-sweep (register cap)
+    // ---- axis-0 slab decomposition (multi-GPU / virtual ranks) ----
+    int nranks = 1, rank = 0;
+    int kg = 0;                         // first replicated level (levels < kg are slabs)
+    long long* flags = nullptr;         // [nranks] arrival counters written by peers
+    long long* cnt = nullptr;           // [2*nranks] send counters, then expected counters
+    double* allpart = nullptr;          // [nranks] residual partial sums, written by peers
+    struct Peer {                       // device pointers of every rank, valid in this process
+        double* P[32];
+        double* F[32];
+        long long* flags;
+        double* allpart;
+    };
+    std::vector<Peer> peers;            // size nranks once connected
+    bool sharded(int k) const { return nranks > 1 && k < kg; }
 };
 
 struct Tile {
@@ -485,12 +582,18 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         return;
     }
     if (D == 3 && E.sweep_variant == 3 && __builtin_popcount(M) > 1 && L.B[2] >= 32 &&
-        L.B[1] >= 8 && L.B[0] >= 128) {
+        L.B[1] >= 8 && L.nblk >= (1L << 21)) {
         using namespace smem_sweep;
         // planes per marching chunk: long chunks amortize the two window
-        // planes each chunk loads twice; short ones keep enough CTAs
-        // (measured on B200: 16 at B0 >= 256, 4 at B0 = 128)
-        const int chunk = E.march_chunk > 0 ? E.march_chunk : (L.B[0] >= 256 ? 16 : 4);
+        // planes each chunk loads twice; short ones keep >= 8 CTAs per SM
+        // in flight (B200 measurements: 16 at 256 planes, 4 at 128)
+        const long tiles = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
+        int chunk = E.march_chunk;
+        if (chunk <= 0) {
+            chunk = 4;
+            for (int c = 16; c >= 8; c >>= 1)
+                if (tiles * ((L.B[0] + c - 1) / c) >= 1184) { chunk = c; break; }
+        }
         dim3 blk(TX, TY, 1);
         dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
         const size_t shm = sizeof(double) * 4 * RING * PL;
@@ -551,6 +654,87 @@ static void launch_pad_fill(Engine& E, int k, long& cnt) {
     ++cnt;
 }
 
+// ---- slab exchanges (no-ops on a single rank) ----
+template <int D>
+static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt) {
+    if (!E.sharded(k)) return;
+    const Lvl& L = E.L[k];
+    const int r = E.rank, P = E.nranks;
+    const unsigned bit0 = 1u << (D - 1);
+    unsigned up = 0, dn = 0;  // q0=0 classes feed the upper neighbor's lower halo
+    for (int c = 0; c < (1 << D); ++c)
+        if ((mask >> c) & 1u) {
+            if (c & bit0) dn |= 1u << c;
+            else up |= 1u << c;
+        }
+    const long n = (long)L.B[1] * (D == 3 ? L.B[2] : 1);
+    const dim3 grid(nb(n, TPB), 1 << D);
+    if (r + 1 < P && up) {
+        k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r + 1].P[k], L, L, L.B[0], 0, up);
+        k_signal<<<1, 1, 0, E.stream>>>(E.peers[r + 1].flags + r, E.cnt + (r + 1));
+        cnt += 2;
+    }
+    if (r > 0 && dn) {
+        k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r - 1].P[k], L, L, 1,
+                                                     L.B[0] + 1, dn);
+        k_signal<<<1, 1, 0, E.stream>>>(E.peers[r - 1].flags + r, E.cnt + (r - 1));
+        cnt += 2;
+    }
+    if (r > 0 && up) {
+        k_wait<<<1, 1, 0, E.stream>>>(E.flags + (r - 1), E.cnt + P + (r - 1));
+        ++cnt;
+    }
+    if (r + 1 < P && dn) {
+        k_wait<<<1, 1, 0, E.stream>>>(E.flags + (r + 1), E.cnt + P + (r + 1));
+        ++cnt;
+    }
+}
+
+// Data-free handshake with both neighbours.  Needed where a halo that was
+// just read in full (by the coarse source term) would otherwise be
+// overwritten by a neighbour's next push before the read finished: the
+// first smoothing half-sweep of a sharded coarse level pushes classes that
+// coarse_src still reads (write-after-read across ranks).
+static void neighbor_barrier(Engine& E, int k, long& cnt) {
+    if (!E.sharded(k)) return;
+    const int r = E.rank, P = E.nranks;
+    for (int q : {r - 1, r + 1}) {
+        if (q < 0 || q >= P) continue;
+        k_signal<<<1, 1, 0, E.stream>>>(E.peers[q].flags + r, E.cnt + q);
+        ++cnt;
+    }
+    for (int q : {r - 1, r + 1}) {
+        if (q < 0 || q >= P) continue;
+        k_wait<<<1, 1, 0, E.stream>>>(E.flags + q, E.cnt + P + q);
+        ++cnt;
+    }
+}
+
+// level kg is replicated: every rank pushes the coarse planes its slab of
+// level kg-1 produced (P and F) into every peer's copy, then pads are filled
+template <int D>
+static void gather_level(Engine& E, int k, long& cnt) {
+    const Lvl& L = E.L[k];
+    const int P = E.nranks, r = E.rank;
+    const int part = L.B[0] / P;  // coarse planes per rank (whole blocks: fine nb even)
+    const int off = r * part;
+    const long n = (long)L.B[1] * (D == 3 ? L.B[2] : 1) * part;
+    const dim3 grid(nb(n, TPB), 1 << D);
+    for (int q = 0; q < P; ++q) {
+        if (q == r) continue;
+        k_push_part<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[q].P[k], L, off, part);
+        k_push_part<D><<<grid, TPB, 0, E.stream>>>(E.F[k], E.peers[q].F[k], L, off, part);
+        k_signal<<<1, 1, 0, E.stream>>>(E.peers[q].flags + r, E.cnt + q);
+        cnt += 3;
+    }
+    for (int q = 0; q < P; ++q) {
+        if (q == r) continue;
+        k_wait<<<1, 1, 0, E.stream>>>(E.flags + q, E.cnt + P + q);
+        ++cnt;
+    }
+    launch_pad_fill<D>(E, k, cnt);
+}
+
 template <int D>
 static void launch_smooth(Engine& E, int k, long& cnt) {
     const Tile t = tile_of(E.L[k]);
@@ -558,11 +742,13 @@ static void launch_smooth(Engine& E, int k, long& cnt) {
         for (unsigned m : E.masks) {
             EA_DISPATCH(D, E.ea, (sweep_mask<D, EA>(E, k, m, t)));
             ++cnt;
+            halo_exchange<D>(E, k, m, cnt);
         }
 }
 
 template <int D>
 static void launch_vcycle(Engine& E, long& cnt) {
+    const unsigned ALL = (1u << (1 << D)) - 1;
     // descent
     for (int k = 0; k < E.nl - 1; ++k) {
         const Lvl& L = E.L[k];
@@ -587,9 +773,12 @@ static void launch_vcycle(Engine& E, long& cnt) {
             cnt += 4;
             launch_pad_fill<D>(E, k + 1, cnt);
         }
+        if (E.sharded(k + 1)) halo_exchange<D>(E, k + 1, ALL, cnt);
+        else if (E.sharded(k)) gather_level<D>(E, k + 1, cnt);
         EA_DISPATCH(D, E.ea, (k_coarse_src_fast<D, EA><<<tc.grid, tc.block, 0, E.stream>>>(
                                  E.P[k + 1], E.F[k + 1], Lc)));
         ++cnt;
+        neighbor_barrier(E, k + 1, cnt);
     }
     launch_smooth<D>(E, E.nl - 1, cnt);  // coarsest: s smoothing steps
     // ascent
@@ -606,6 +795,7 @@ static void launch_vcycle(Engine& E, long& cnt) {
             ++cnt;
             launch_pad_fill<D>(E, k, cnt);
         }
+        halo_exchange<D>(E, k, ALL, cnt);
         launch_smooth<D>(E, k, cnt);
     }
 }
@@ -618,6 +808,24 @@ static void launch_norm(Engine& E, long& cnt) {
                              E.P[0], E.F[0], L, E.part)));
     k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, E.npart, E.dsum);
     cnt += 2;
+    if (E.nranks > 1) {  // fixed rank-order sum of the partials on every rank
+        const int P = E.nranks, r = E.rank;
+        for (int q = 0; q < P; ++q) {
+            k_put_partial<<<1, 1, 0, E.stream>>>(E.dsum, E.peers[q].allpart + r);
+            ++cnt;
+            if (q != r) {
+                k_signal<<<1, 1, 0, E.stream>>>(E.peers[q].flags + r, E.cnt + q);
+                ++cnt;
+            }
+        }
+        for (int q = 0; q < P; ++q)
+            if (q != r) {
+                k_wait<<<1, 1, 0, E.stream>>>(E.flags + q, E.cnt + P + q);
+                ++cnt;
+            }
+        k_sum_partials<<<1, 1, 0, E.stream>>>(E.allpart, P, E.dsum);
+        ++cnt;
+    }
 }
 
 static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* ex) {
@@ -668,6 +876,8 @@ static Lvl make_lvl(int dim, const int* n, int ea, double dmin, double dmax, dou
         L.cls = pitch * L.E[0];
     }
     L.cls = (L.cls + 31) / 32 * 32;  // 256-byte aligned class arrays
+    L.off0 = 0;
+    L.G0 = L.B[0];
     // scalars exactly as the reference computes them (PKG/grid.py:71-73,
     // PKG/smoothers.py:143-144, PKG/stencil.py:37-38,58)
     L.h = (dmax - dmin) / n[0];
@@ -690,10 +900,14 @@ extern "C" {
 
 // masks: one uint32 per color group (classes updated after one ghost
 // refresh); the smoother of one smoothing step runs them in order.
-void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dmax,
-                          int mesh_level, double a, double b, const int* kinds,
-                          const double* vals, int nmasks, const unsigned* masks, int s,
-                          void* stream) {
+// Create an engine.  nranks > 1: this engine owns the axis-0 slab `rank` of
+// every level whose block-plane count divides evenly into >= min_planes
+// (even) planes per rank; coarser levels are replicated on every rank.  Peer
+// pointers are supplied later by fasmg_engine_connect.
+void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, double dmax,
+                               int mesh_level, double a, double b, const int* kinds,
+                               const double* vals, int nmasks, const unsigned* masks, int s,
+                               void* stream, int nranks, int rank, int min_planes) {
     if (dim != 2 && dim != 3) { fasmg_set_error(FASMG_EINVAL, "dim must be 2 or 3"); return nullptr; }
     if (mesh_level < 1 || mesh_level > 30) { fasmg_set_error(FASMG_EINVAL, "bad mesh_level"); return nullptr; }
     for (int t = 0; t < dim; ++t)
@@ -701,12 +915,23 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
             fasmg_set_error(FASMG_EINVAL, "grid does not stay even through mesh_level coarsenings");
             return nullptr;
         }
+    if (nranks < 1 || rank < 0 || rank >= nranks) {
+        fasmg_set_error(FASMG_EINVAL, "bad nranks/rank");
+        return nullptr;
+    }
+    if (nranks > 1 && (ea >= 0 || kinds[0] == BC_PERIODIC)) {
+        fasmg_set_error(FASMG_EINVAL,
+                        "slab decomposition supports cell-centered fields without periodic x");
+        return nullptr;
+    }
     Engine* E = new Engine();
     E->dim = dim;
     E->ea = ea;
     E->nl = mesh_level + 1;
     E->s = s;
     E->stream = (cudaStream_t)stream;
+    E->nranks = nranks;
+    E->rank = rank;
     for (int t = 0; t < 3; ++t)
         for (int sd = 0; sd < 2; ++sd) {
             E->bc.kind[t][sd] = t < dim ? kinds[2 * t + sd] : 0;
@@ -725,9 +950,34 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
     if (const char* v = getenv("FASMG_MARCH_CHUNK")) E->march_chunk = std::max(0, atoi(v));
     if (const char* v = getenv("FASMG_TILE_Y")) g_tile_y = std::max(1, atoi(v));
     if (const char* v = getenv("FASMG_SWEEP_MINB")) E->sweep_minb = atoi(v);
+    // sharded levels: a prefix of the hierarchy, never the coarsest
+    E->kg = 0;
+    if (nranks > 1) {
+        const int mp = std::max(2, min_planes);
+        for (int k = 0; k < E->nl - 1; ++k) {
+            const int B0 = (n[0] >> k) / 2;
+            if (B0 % nranks || (B0 / nranks) % 2 || B0 / nranks < mp) break;
+            E->kg = k + 1;
+        }
+        if (E->kg == 0) {
+            fasmg_set_error(FASMG_EINVAL, "grid too small to split into slabs");
+            delete E;
+            return nullptr;
+        }
+    }
     int nn[3] = {n[0], n[1], dim == 3 ? n[2] : 2};
     for (int k = 0; k < E->nl; ++k) {
-        E->L[k] = make_lvl(dim, nn, ea, dmin, dmax, a, b);
+        Lvl L = make_lvl(dim, nn, ea, dmin, dmax, a, b);
+        if (E->sharded(k)) {  // local slab: nb planes + the two halo/pad planes
+            const int nbp = L.B[0] / nranks;
+            L.off0 = rank * nbp;
+            L.G0 = L.B[0];
+            L.B[0] = nbp;
+            L.E[0] = nbp + 2;
+            L.nblk = (long)nbp * L.B[1] * (dim == 3 ? L.B[2] : 1);
+            L.cls = (L.s0 * L.E[0] + 31) / 32 * 32;
+        }
+        E->L[k] = L;
         size_t bytes = sizeof(double) * (size_t)E->L[k].cls * (1u << dim);
         if (fasmg_check(cudaMalloc(&E->P[k], bytes)) || fasmg_check(cudaMalloc(&E->F[k], bytes))) {
             delete E;
@@ -746,13 +996,103 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
     E->npart = (int)tile_ctas(tile_of(E->L[0]));
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
-        fasmg_check(cudaMallocHost(&E->hsum, sizeof(double)))) {
+        fasmg_check(cudaMallocHost(&E->hsum, sizeof(double))) ||
+        fasmg_check(cudaMalloc(&E->flags, sizeof(long long) * nranks)) ||
+        fasmg_check(cudaMalloc(&E->cnt, sizeof(long long) * 2 * nranks)) ||
+        fasmg_check(cudaMalloc(&E->allpart, sizeof(double) * nranks))) {
         delete E;
         return nullptr;
+    }
+    cudaMemsetAsync(E->flags, 0, sizeof(long long) * nranks, E->stream);
+    cudaMemsetAsync(E->cnt, 0, sizeof(long long) * 2 * nranks, E->stream);
+    cudaMemsetAsync(E->allpart, 0, sizeof(double) * nranks, E->stream);
+    if (nranks == 1) {
+        Engine::Peer me;
+        for (int k = 0; k < 32; ++k) { me.P[k] = E->P[k]; me.F[k] = E->F[k]; }
+        me.flags = E->flags;
+        me.allpart = E->allpart;
+        E->peers.assign(1, me);
     }
     if (fasmg_check(cudaStreamSynchronize(E->stream))) { delete E; return nullptr; }
     return E;
 }
+
+void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dmax,
+                          int mesh_level, double a, double b, const int* kinds,
+                          const double* vals, int nmasks, const unsigned* masks, int s,
+                          void* stream) {
+    return fasmg_engine_create_slab(dim, n, ea, dmin, dmax, mesh_level, a, b, kinds, vals,
+                                    nmasks, masks, s, stream, 1, 0, 0);
+}
+
+// Number of device pointers fasmg_engine_export writes: P[0..nl), F[0..nl),
+// flags, allpart.
+int fasmg_engine_export_count(void* h) { return 2 * ((Engine*)h)->nl + 2; }
+
+int fasmg_engine_export(void* h, unsigned long long* out) {
+    Engine* E = (Engine*)h;
+    int t = 0;
+    for (int k = 0; k < E->nl; ++k) out[t++] = (unsigned long long)E->P[k];
+    for (int k = 0; k < E->nl; ++k) out[t++] = (unsigned long long)E->F[k];
+    out[t++] = (unsigned long long)E->flags;
+    out[t++] = (unsigned long long)E->allpart;
+    return 0;
+}
+
+// all: nranks consecutive export arrays, pointers valid in THIS process
+// (the peer's own pointers for virtual ranks on one device; CUDA-IPC
+// mappings for one process per GPU)
+int fasmg_engine_connect(void* h, const unsigned long long* all, int nranks) {
+    Engine* E = (Engine*)h;
+    if (nranks != E->nranks) return fasmg_set_error(FASMG_EINVAL, "nranks mismatch");
+    const int per = 2 * E->nl + 2;
+    E->peers.assign(nranks, Engine::Peer());
+    for (int r = 0; r < nranks; ++r) {
+        const unsigned long long* x = all + (long)r * per;
+        Engine::Peer& pr = E->peers[r];
+        for (int k = 0; k < 32; ++k) { pr.P[k] = nullptr; pr.F[k] = nullptr; }
+        for (int k = 0; k < E->nl; ++k) {
+            pr.P[k] = (double*)x[k];
+            pr.F[k] = (double*)x[E->nl + k];
+        }
+        pr.flags = (long long*)x[2 * E->nl];
+        pr.allpart = (double*)x[2 * E->nl + 1];
+    }
+    return 0;
+}
+
+// [kg, local planes of level 0, global offset of level 0]
+int fasmg_engine_slab_info(void* h, int* out) {
+    Engine* E = (Engine*)h;
+    out[0] = E->kg;
+    out[1] = E->L[0].B[0];
+    out[2] = E->L[0].off0;
+    return 0;
+}
+
+// full halo exchange of level 0 (after loading a slab)
+int fasmg_engine_sync_halos(void* h) {
+    Engine* E = (Engine*)h;
+    long cnt = 0;
+    if (E->dim == 3) halo_exchange<3>(*E, 0, 0xFFu, cnt);
+    else halo_exchange<2>(*E, 0, 0xFu, cnt);
+    return fasmg_check_launch();
+}
+
+int fasmg_ipc_get_handle(void* ptr, unsigned char* out64) {
+    cudaIpcMemHandle_t hd;
+    int st = fasmg_check(cudaIpcGetMemHandle(&hd, ptr));
+    if (!st) memcpy(out64, &hd, sizeof(hd));
+    return st;
+}
+
+int fasmg_ipc_open_handle(const unsigned char* in64, void** ptr) {
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, in64, sizeof(hd));
+    return fasmg_check(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int fasmg_ipc_close_handle(void* ptr) { return fasmg_check(cudaIpcCloseMemHandle(ptr)); }
 
 void fasmg_engine_destroy(void* h) {
     Engine* E = (Engine*)h;
@@ -771,6 +1111,9 @@ void fasmg_engine_destroy(void* h) {
     cudaFree(E->part);
     cudaFree(E->dsum);
     cudaFreeHost(E->hsum);
+    cudaFree(E->flags);
+    cudaFree(E->cnt);
+    cudaFree(E->allpart);
     delete E;
 }
 
@@ -781,6 +1124,7 @@ int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double
     const Lvl& L = E->L[0];
     int e[3];
     for (int a = 0; a < 3; ++a) e[a] = a < E->dim ? (a == E->ea ? L.n[a] + 1 : L.n[a] + 2) : 1;
+    if (E->sharded(0)) e[0] = 2 * L.B[0] + 2;  // rank-local slab (+1 ghost plane each side)
     long tot = (long)e[0] * e[1] * e[2];
     if (E->dim == 3) {
         k_pack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(pcore, ps[0], ps[1], ps[2], E->P[0], L,
@@ -805,6 +1149,7 @@ int fasmg_engine_store(void* h, double* pcore, const long* ps) {
     const Lvl& L = E->L[0];
     int m[3];
     for (int a = 0; a < 3; ++a) m[a] = a < E->dim ? (a == E->ea ? L.n[a] - 1 : L.n[a]) : 1;
+    if (E->sharded(0)) m[0] = 2 * L.B[0];
     long tot = (long)m[0] * m[1] * m[2];
     if (E->dim == 3)
         k_unpack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], ps[2],
@@ -847,6 +1192,49 @@ int fasmg_engine_run(void* h, int count, int with_norm, double* sumsq, int use_g
         *sumsq = *E->hsum;
     }
     return 0;
+}
+
+// Asynchronous variant for ranks that must run concurrently (virtual ranks
+// on one device, whose graphs wait on each other): enqueue `count` V-cycles
+// (+ norm) and return; fasmg_engine_result waits and reads the last sum.
+int fasmg_engine_launch(void* h, int count, int with_norm) {
+    Engine* E = (Engine*)h;
+    int st;
+    for (int it = 0; it < count; ++it) {
+        cudaGraphExec_t* ex = with_norm ? &E->exec_vn : &E->exec_v;
+        cudaGraph_t* g = with_norm ? &E->graph_vn : &E->graph_v;
+        if (!*ex && (st = capture(*E, with_norm != 0, g, ex))) return st;
+        if ((st = fasmg_check(cudaGraphLaunch(*ex, E->stream)))) return st;
+    }
+    return 0;
+}
+
+int fasmg_engine_result(void* h, double* sumsq) {
+    Engine* E = (Engine*)h;
+    int st = fasmg_check(cudaStreamSynchronize(E->stream));
+    if (!st) *sumsq = *E->hsum;
+    return st;
+}
+
+// Debug/test access to a level's blocked arrays: geometry
+// [cls, s0, s1, E0, E1, E2, B0(local), off0, G0] and a raw device copy.
+int fasmg_engine_level_geom(void* h, int k, long* out) {
+    Engine* E = (Engine*)h;
+    if (k < 0 || k >= E->nl) return fasmg_set_error(FASMG_EINVAL, "level out of range");
+    const Lvl& L = E->L[k];
+    long v[9] = {L.cls, L.s0, L.s1, L.E[0], L.E[1], L.E[2], L.B[0], L.off0, L.G0};
+    for (int t = 0; t < 9; ++t) out[t] = v[t];
+    return 0;
+}
+
+int fasmg_engine_level_copy(void* h, int k, int which, double* dst) {
+    Engine* E = (Engine*)h;
+    if (k < 0 || k >= E->nl) return fasmg_set_error(FASMG_EINVAL, "level out of range");
+    const double* src = which == 0 ? E->P[k] : E->F[k];
+    int st = fasmg_check(cudaStreamSynchronize(E->stream));
+    if (st) return st;
+    return fasmg_check(cudaMemcpy(dst, src, sizeof(double) * E->L[k].cls * (1u << E->dim),
+                                  cudaMemcpyDeviceToDevice));
 }
 
 // Residual sum of squares of the current finest state (no V-cycle).

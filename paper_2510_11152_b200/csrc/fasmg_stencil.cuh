@@ -46,11 +46,17 @@ __device__ __forceinline__ bool tile_coords(const Lvl& L, int* bb) {
     return bb[0] <= L.B[0] && bb[1] <= L.B[1];
 }
 
+// global block index along axis 0 (slab decomposition: local + offset)
+__device__ __forceinline__ int gb0(const Lvl& L, const int* bb) { return bb[0] + L.off0; }
+
+// is the block on the GLOBAL boundary of the level?  (axis 0 uses the
+// global index, so internal slab faces are not boundaries)
 template <int D>
 __device__ __forceinline__ bool on_boundary(const Lvl& L, const int* bb) {
-    bool r = false;
+    const int g = gb0(L, bb);
+    bool r = g == 1 || g == L.G0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) r = r || bb[a] == 1 || bb[a] == L.B[a];
+    for (int a = 1; a < D; ++a) r = r || bb[a] == 1 || bb[a] == L.B[a];
     return r;
 }
 
@@ -58,7 +64,9 @@ __device__ __forceinline__ bool on_boundary(const Lvl& L, const int* bb) {
 template <int D, int EA>
 __device__ __forceinline__ bool is_wall(const Lvl& L, int c, const int* bb) {
     if (EA < 0) return false;
-    return qbit<D>(c, EA) == 0 && bb[EA] == L.B[EA];
+    const int g = EA == 0 ? gb0(L, bb) : bb[EA];
+    const int B = EA == 0 ? L.G0 : L.B[EA];
+    return qbit<D>(c, EA) == 0 && g == B;
 }
 
 // sum of the 2d neighbors of point (c, o) in the reference order
@@ -92,23 +100,24 @@ __device__ __forceinline__ void write_pads(double* __restrict__ P, const Lvl& L,
         const long dcls = (long)((c ^ bit) - c) * L.cls;
         const long sa = bstride<D>(L, a);
         const bool q = (c & bit) != 0;
-        const int B = L.B[a];
+        const int B = a == 0 ? L.G0 : L.B[a];   // global extent (axis 0 may be a slab)
+        const int g = a == 0 ? gb0(L, bb) : bb[a];
         if (a != EA) {
-            if (q && bb[a] == 1) {
+            if (q && g == 1) {
                 const int k = bc.kind[a][0];
                 if (k == BC_DIRICHLET) P[o + dcls - sa] = sb(ml(2.0, bc.val[a][0]), v);
                 else if (k == BC_NEUMANN) P[o + dcls - sa] = v;
                 else P[o + (long)B * sa] = v;  // periodic: hi ghost x=n+1 <- p(1)
             }
-            if (!q && bb[a] == B) {
+            if (!q && g == B) {
                 const int k = bc.kind[a][1];
                 if (k == BC_DIRICHLET) P[o + dcls + sa] = sb(ml(2.0, bc.val[a][1]), v);
                 else if (k == BC_NEUMANN) P[o + dcls + sa] = v;
                 else P[o - (long)B * sa] = v;  // periodic: lo ghost x=0 <- p(n)
             }
         } else {
-            if (q && bb[a] == 1 && bc.kind[a][0] == BC_NEUMANN) P[o + dcls - sa] = v;
-            if (q && bb[a] == B && bc.kind[a][1] == BC_NEUMANN) P[o + dcls] = v;
+            if (q && g == 1 && bc.kind[a][0] == BC_NEUMANN) P[o + dcls - sa] = v;
+            if (q && g == B && bc.kind[a][1] == BC_NEUMANN) P[o + dcls] = v;
         }
     }
 }
@@ -129,6 +138,8 @@ __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
     long n1 = L.B[oth[0]], n2 = (D == 3) ? L.B[oth[1]] : 1;
     long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (t >= n1 * n2) return;
+    if (a == 0 && ((side == 0 && L.off0 != 0) || (side == 1 && L.off0 + L.B[0] != L.G0)))
+        return;  // internal slab face: the halo comes from the neighbor rank
     int bb[3] = {0, 0, 0};
     bb[a] = side ? L.B[a] : 1;
     if (D == 3) {
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(256) k_sweep_march(double* __restrict__ P,
             }
             nv[c] = dv(ad(ml(L.h2, fv[c]), ml(L.b, ns)), L.denom);
         }
-        const bool bnd = bnd_col || b0 == 1 || b0 == L.B[0];
+        const bool bnd = bnd_col || b0 + L.off0 == 1 || b0 + L.off0 == L.G0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             if (!((MASK >> c) & 1u)) continue;
@@ -511,8 +522,7 @@ __global__ void __launch_bounds__(256) k_sweep_smem(double* __restrict__ P,
 #pragma unroll
             for (int c = 0; c < NC; ++c)
                 if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
-            const bool bnd = bb[0] == 1 || bb[0] == L.B[0] || bb[1] == 1 || bb[1] == L.B[1] ||
-                             bb[2] == 1 || bb[2] == L.B[2];
+            const bool bnd = on_boundary<3>(L, bb);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 if (!((MASK >> c) & 1u)) continue;
@@ -541,6 +551,21 @@ __device__ __forceinline__ double op_fast(const double* __restrict__ P, const Lv
     return sb(ml(L.a, cv), ml(L.b, lap));
 }
 
+// coarse cell of fine block bb: the fine block's GLOBAL index I is the
+// coarse cell index; coarse class bit I&1, coarse block (I+1)>>1, made
+// local to the coarse level's slab (Lc.off0)
+template <int D>
+__device__ __forceinline__ void coarse_of(const Lvl& L, const Lvl& Lc, const int* bb, int& cc,
+                                          int* cb) {
+    cc = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int I = a == 0 ? gb0(L, bb) : bb[a];
+        cc |= (I & 1) << (D - 1 - a);
+        cb[a] = ((I + 1) >> 1) - (a == 0 ? Lc.off0 : 0);
+    }
+}
+
 // ----------------------------------------------------------- tau kernel
 // Cell-centered fine level k -> coarse level k+1 in one pass: residual at the
 // 2^d children of coarse cell bb, restriction of r and p (lexicographic child
@@ -554,23 +579,47 @@ __global__ void __launch_bounds__(256) k_tau_fast(const double* __restrict__ P,
                                                   double* __restrict__ Fc, Lvl Lc, BcSpec bc) {
     int bb[3];
     if (!tile_coords<D>(L, bb)) return;
+    constexpr int NC = 1 << D;
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+    // phase 1: all loads (2^d centers, 2^d f, and the d*2^(d-1) neighbors
+    // outside the block) before any arithmetic
+    double pc[NC], fv[NC], out[NC][D];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const long o = o0 + (long)c * L.cls;
+        pc[c] = __ldg(P + o);
+        fv[c] = __ldg(F + o);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int bit = 1 << (D - 1 - a);
+            const long dcls = (long)((c ^ bit) - c) * L.cls;
+            const long sa = bstride<D>(L, a);
+            // the neighbor across the block face: W of q=1, E of q=0
+            out[c][a] = (c & bit) ? __ldg(P + o + dcls - sa) : __ldg(P + o + dcls + sa);
+        }
+    }
+    // phase 2: residual at every child in the reference order, restriction
+    // in lexicographic child order (descending class id)
     double rp = 0.0, rr = 0.0;
 #pragma unroll
-    for (int c = (1 << D) - 1; c >= 0; --c) {
-        const long o = o0 + (long)c * L.cls;
-        const double pv = P[o];
-        const double r = sb(F[o], op_fast<D>(P, L, c, o));
-        if (c == (1 << D) - 1) { rp = pv; rr = r; }
-        else { rp = ad(rp, pv); rr = ad(rr, r); }
+    for (int c = NC - 1; c >= 0; --c) {
+        double ns = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int bit = 1 << (D - 1 - a);
+            const double inside = pc[c ^ bit];
+            const double e = (c & bit) ? inside : out[c][a];
+            const double w = (c & bit) ? out[c][a] : inside;
+            ns = a == 0 ? ad(e, w) : ad(ad(ns, e), w);
+        }
+        const double lap = ml(sb(ns, ml(D == 3 ? 6.0 : 4.0, pc[c])), L.inv_h2);
+        const double r = sb(fv[c], sb(ml(L.a, pc[c]), ml(L.b, lap)));
+        if (c == NC - 1) { rp = pc[c]; rr = r; }
+        else { rp = ad(rp, pc[c]); rr = ad(rr, r); }
     }
     const double sc = D == 3 ? 0.125 : 0.25;
     int cc = 0, cb[3] = {0, 0, 0};
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-        cc |= (bb[a] & 1) << (D - 1 - a);
-        cb[a] = (bb[a] + 1) >> 1;
-    }
+    coarse_of<D>(L, Lc, bb, cc, cb);
     const long oc = at<D>(Lc, cc, cb[0], cb[1], cb[2]);
     const double pcv = ml(rp, sc);
     Pc[oc] = pcv;
@@ -612,11 +661,7 @@ __global__ void __launch_bounds__(256) k_correct_fast(double* __restrict__ P, Lv
     }
     rp = ml(rp, D == 3 ? 0.125 : 0.25);
     int cc = 0, cb[3] = {0, 0, 0};
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-        cc |= (bb[a] & 1) << (D - 1 - a);
-        cb[a] = (bb[a] + 1) >> 1;
-    }
+    coarse_of<D>(L, Lc, bb, cc, cb);
     const double corr = sb(Pc[at<D>(Lc, cc, cb[0], cb[1], cb[2])], rp);
     const bool bnd = on_boundary<D>(L, bb);
 #pragma unroll

@@ -1,0 +1,320 @@
+"""Axis-0 slab decomposition of the FAS solver across GPUs.
+
+Each rank's native engine owns the slab ``rank`` (a contiguous range of
+block planes along array axis 0, the outermost axis of the C-order layout)
+of every level whose plane count splits evenly into enough planes per rank;
+coarser levels are replicated and solved redundantly on every rank (same
+inputs, same results, no scatter).  Inside the V-cycle graph:
+
+* after every smoothing half-sweep the updated classes' boundary planes are
+  stored straight into the neighbours' halo planes (CUDA P2P / IPC peer
+  memory over NVLink) and published with system-scope release/acquire
+  counters -- one exchange per color sweep, as the north star asks;
+* after the restriction the coarse slab halos, or -- at the first replicated
+  level -- the whole coarse level, are exchanged the same way (all-gather);
+* the outer residual's sum of squares is reduced in fixed rank order.
+
+Fields and residual histories equal the single-GPU solve: every per-point
+value is computed from identical inputs in identical order (bitwise); only
+the norm's summation order differs (~1e-16 relative).
+
+Two front ends share the engine:
+
+* :class:`VirtualSlabSolver` -- P slabs on ONE device in one process, each
+  with its own stream; same kernels, same peer-store/counter protocol
+  (the "virtual ranks" test of SURVEY.md §4 item 3a);
+* :class:`DistSlabSolver` -- one process per GPU (torch.distributed for the
+  rendezvous): each rank exports its level arrays as CUDA IPC handles, maps
+  its peers', and runs its own graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _native as N
+from .boundary import BoundaryCondition, fill_ghosts
+from .errors import NativeError
+from .fas import FasParams, SolveReport
+from .grid import Field, GridHierarchy, Location, subtract_interior_mean
+from .smoothers import SweepPlan
+from .stencil import OperatorCoeffs
+
+
+def slab_cells(n0: int, nranks: int, rank: int):
+    """1-based inclusive range of axis-0 cells owned by ``rank`` at the
+    finest level (block planes are pairs of cells)."""
+    B0 = n0 // 2
+    if B0 % nranks:
+        raise ValueError(f"{B0} block planes do not split over {nranks} ranks")
+    nb = B0 // nranks
+    return 2 * rank * nb + 1, 2 * (rank + 1) * nb
+
+
+def slab_view(data: torch.Tensor, halo: int, n0: int, nranks: int, rank: int) -> torch.Tensor:
+    """The rank's cells along axis 0 plus one ghost plane on each side, as a
+    view of the global C-order data array (core index 0 at data g-1)."""
+    lo, hi = slab_cells(n0, nranks, rank)
+    return data[halo - 1 + lo - 1: halo - 1 + hi + 2]
+
+
+class _SlabEngine:
+    def __init__(self, hierarchy: GridHierarchy, location: Location, bc: BoundaryCondition,
+                 plan: SweepPlan, coeffs: OperatorCoeffs, s: int, nranks: int, rank: int,
+                 device: torch.device, min_planes: int = 4, stream=None):
+        if location is not Location.CELL:
+            raise NativeError("slab decomposition supports cell-centered fields")
+        g = hierarchy.fine
+        kinds, vals = bc.codes()
+        masks = plan.class_masks()
+        self.device = device
+        if stream is None:
+            with torch.cuda.device(device):
+                stream = ctypes.c_void_p()
+                N.check(N.lib().fasmg_stream_create(ctypes.byref(stream)))
+            self._own_stream = True
+        else:
+            self._own_stream = False
+        self.stream = stream
+        with torch.cuda.device(device):
+            h = N.lib().fasmg_engine_create_slab(
+                g.dim, N.ints(g.shape), -1, float(g.domain_min[0]), float(g.domain_max[0]),
+                hierarchy.mesh_level, float(coeffs.a), float(coeffs.b), N.ints(kinds),
+                N.doubles(vals), len(masks), (ctypes.c_uint * len(masks))(*masks), int(s),
+                self.stream, int(nranks), int(rank), int(min_planes))
+        if not h:
+            raise NativeError("fasmg_engine_create_slab failed: "
+                              + N.lib().fasmg_last_error().decode(errors="replace"))
+        self.handle = ctypes.c_void_p(h)
+        self.nranks, self.rank = nranks, rank
+        self.n0 = g.shape[0]
+        info = (ctypes.c_int * 3)()
+        N.call("fasmg_engine_slab_info", self.handle, info)
+        self.kg, self.planes, self.off0 = info[0], info[1], info[2]
+
+    def export(self):
+        cnt = N.lib().fasmg_engine_export_count(self.handle)
+        arr = (ctypes.c_ulonglong * cnt)()
+        N.check(N.lib().fasmg_engine_export(self.handle, arr))
+        return list(arr)
+
+    def connect(self, all_exports):
+        flat = [x for e in all_exports for x in e]
+        arr = (ctypes.c_ulonglong * len(flat))(*flat)
+        N.check(N.lib().fasmg_engine_connect(self.handle, arr, len(all_exports)))
+
+    def load(self, pv: torch.Tensor, fv: torch.Tensor, halo_p: int, halo_f: int):
+        """Pack slab views (rank cells + 1 ghost plane each side along axis 0)."""
+        def core(v, g):
+            return v[(slice(None),) + tuple(slice(g - 1, v.shape[a] - (g - 1))
+                                            for a in range(1, v.dim()))]
+        pc, fc = core(pv, halo_p), core(fv, halo_f)
+        N.wait(self.stream, N.torch_stream())
+        N.call("fasmg_engine_load", self.handle, N.ptr(pc), N.strides(pc), N.ptr(fc),
+               N.strides(fc))
+
+    def store(self, pv: torch.Tensor, halo_p: int):
+        pc = pv[(slice(None),) + tuple(slice(halo_p - 1, pv.shape[a] - (halo_p - 1))
+                                        for a in range(1, pv.dim()))]
+        N.call("fasmg_engine_store", self.handle, N.ptr(pc), N.strides(pc))
+        N.wait(N.torch_stream(), self.stream)
+
+    def sync_halos(self):
+        N.call("fasmg_engine_sync_halos", self.handle)
+
+    def launch(self, count: int, with_norm: bool):
+        N.call("fasmg_engine_launch", self.handle, int(count), 1 if with_norm else 0)
+
+    def result(self) -> float:
+        out = ctypes.c_double()
+        N.call("fasmg_engine_result", self.handle, ctypes.byref(out))
+        return out.value
+
+    def synchronize(self):
+        N.call("fasmg_stream_synchronize", self.stream)
+
+    def time_sweeps(self, level: int = 0, reps: int = 20) -> float:
+        ms = ctypes.c_double()
+        N.call("fasmg_engine_time_sweeps", self.handle, int(level), int(reps), ctypes.byref(ms))
+        return ms.value
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and N._lib is not None:
+            N.lib().fasmg_engine_destroy(self.handle)
+            self.handle = None
+            if self._own_stream:
+                N.lib().fasmg_stream_destroy(self.stream)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class VirtualSlabSolver:
+    """``parts`` slab engines on one device (separate streams), exchanging
+    halos through the same peer-store/counter protocol as real ranks."""
+
+    def __init__(self, hierarchy: GridHierarchy, location: Location, bc: BoundaryCondition,
+                 plan: SweepPlan, coeffs: OperatorCoeffs, parts: int, min_planes: int = 4):
+        self.hierarchy, self.location, self.bc = hierarchy, location, bc
+        self.plan, self.coeffs, self.parts, self.min_planes = plan, coeffs, parts, min_planes
+        self._engines = {}
+
+    def engines(self, s: int, device: torch.device):
+        key = (int(s), device.index)
+        es = self._engines.get(key)
+        if es is None:
+            es = [_SlabEngine(self.hierarchy, self.location, self.bc, self.plan, self.coeffs,
+                              s, self.parts, r, device, self.min_planes)
+                  for r in range(self.parts)]
+            exports = [e.export() for e in es]
+            for e in es:
+                e.connect(exports)
+            self._engines[key] = es
+        return es
+
+    def _singular(self):
+        return self.coeffs.a == 0.0 and all(r.kind != "dirichlet" for _, r in self.bc.faces)
+
+    def _load(self, es, p: Field, f: Field):
+        n0 = p.grid.shape[0]
+        for e in es:
+            e.load(slab_view(p.data, p.halo, n0, self.parts, e.rank),
+                   slab_view(f.data, f.halo, n0, self.parts, e.rank), p.halo, f.halo)
+        for e in es:
+            e.synchronize()
+        for e in es:
+            e.sync_halos()
+
+    def _store(self, es, p: Field):
+        n0 = p.grid.shape[0]
+        for e in es:
+            v = slab_view(p.data, p.halo, n0, self.parts, e.rank)
+            e.store(v, p.halo)
+
+    def vcycle(self, p: Field, f: Field, s: int) -> Field:
+        es = self.engines(s, p.device)
+        self._load(es, p, f)
+        for e in es:
+            e.launch(1, False)
+        for e in es:
+            e.synchronize()
+        self._store(es, p)
+        p.ghosts_fresh = False
+        return p
+
+    def solve(self, p: Field, f: Field, params: FasParams) -> SolveReport:
+        singular = self._singular()
+        if singular:
+            subtract_interior_mean(f)
+        es = self.engines(params.s, p.device)
+        self._load(es, p, f)
+        g = self.hierarchy.fine
+        scale = g.h ** (g.dim / 2.0)
+        history = []
+        for _ in range(params.k_max):
+            for e in es:
+                e.launch(1, True)
+            sums = [e.result() for e in es]
+            if any(x != sums[0] for x in sums):
+                raise NativeError(f"ranks disagree on the residual: {sums}")
+            res = scale * math.sqrt(sums[0])
+            history.append(res)
+            if res <= params.tol:
+                break
+        self._store(es, p)
+        fill_ghosts(p, self.bc)
+        if singular:
+            subtract_interior_mean(p)
+            p.ghosts_fresh = False
+        return SolveReport(len(history), history, bool(history and history[-1] <= params.tol))
+
+
+def exchange_ipc(engine_exports, handle_of, open_handle, all_gather_object, rank, world):
+    """Turn this rank's exported device pointers into every rank's pointers
+    valid in this process: export CUDA-IPC handles, all-gather them,
+    open the peers'.  The callables are injected so the host-side protocol
+    is testable without GPUs (tests/test_slab_cpu.py)."""
+    mine = [handle_of(ptr) for ptr in engine_exports]
+    gathered = [None] * world
+    all_gather_object(gathered, mine)
+    out = []
+    for r in range(world):
+        if r == rank:
+            out.append(list(engine_exports))
+        else:
+            out.append([open_handle(hd) for hd in gathered[r]])
+    return out
+
+
+class DistSlabSolver:
+    """One process per GPU: rank ``rank`` of ``world`` owns its slab; the
+    caller passes rank-local slab views (its cells plus one ghost plane on
+    each side along axis 0) of the global p and f."""
+
+    def __init__(self, hierarchy: GridHierarchy, location: Location, bc: BoundaryCondition,
+                 plan: SweepPlan, coeffs: OperatorCoeffs, s: int, device: torch.device,
+                 group=None, min_planes: int = 4):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.hierarchy, self.bc, self.coeffs = hierarchy, bc, coeffs
+        self.engine = _SlabEngine(hierarchy, location, bc, plan, coeffs, s, self.world,
+                                  self.rank, device, min_planes)
+        self._opened = []
+
+        def handle_of(ptr):
+            buf = ctypes.create_string_buffer(64)
+            N.check(N.lib().fasmg_ipc_get_handle(ctypes.c_void_p(ptr), buf))
+            return buf.raw
+
+        def open_handle(hd):
+            out = ctypes.c_void_p()
+            N.check(N.lib().fasmg_ipc_open_handle(hd, ctypes.byref(out)))
+            self._opened.append(out.value)
+            return out.value
+
+        with torch.cuda.device(device):
+            ptrs = exchange_ipc(self.engine.export(), handle_of, open_handle,
+                                lambda out, obj: dist.all_gather_object(out, obj, group=group),
+                                self.rank, self.world)
+        self.engine.connect(ptrs)
+        dist.barrier(group=group)
+
+    def load(self, pv: torch.Tensor, fv: torch.Tensor, halo_p: int = 1, halo_f: int = 1):
+        self.engine.load(pv, fv, halo_p, halo_f)
+        self.engine.synchronize()
+        self.dist.barrier(group=self.group)
+        self.engine.sync_halos()
+
+    def run(self, count: int = 1) -> float:
+        """``count`` V-cycles, each followed by the global residual norm."""
+        for _ in range(count):
+            self.engine.launch(1, True)
+        sumsq = self.engine.result()
+        g = self.hierarchy.fine
+        return g.h ** (g.dim / 2.0) * math.sqrt(sumsq)
+
+    def solve_loaded(self, params: FasParams) -> SolveReport:
+        history = []
+        for _ in range(params.k_max):
+            res = self.run(1)
+            history.append(res)
+            if res <= params.tol:
+                break
+        return SolveReport(len(history), history, bool(history and history[-1] <= params.tol))
+
+    def store(self, pv: torch.Tensor, halo_p: int = 1):
+        self.engine.store(pv, halo_p)
+
+    def close(self):
+        for ptr in self._opened:
+            N.lib().fasmg_ipc_close_handle(ctypes.c_void_p(ptr))
+        self._opened = []
+        self.engine.close()
