@@ -358,7 +358,7 @@ def b200_arm(args):
             pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": ("k_sweep_smem" if dim == 3 else "k_sweep_fast")
+                "kernel": ("k_sweep_tma" if dim == 3 else "k_sweep_fast")
                           + " (finest-level X-MCGS half-sweep)",
                 "kernel_ms": sweep_ms,
                 "algorithmic_bytes_per_launch": BYTES_PER_DOF_HALF_SWEEP * local_dof,

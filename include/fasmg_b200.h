@@ -160,6 +160,11 @@ long fasmg_engine_kernels_per_vcycle(void* engine, int with_norm);
  * half-sweep launch on `level`, over `reps` launches */
 int fasmg_engine_time_sweeps(void* engine, int level, int reps, double* ms);
 int fasmg_engine_level_info(void* engine, int level, long* info);
+/* debug: run level `level`'s first wavefront smoothing launch with a trace
+ * of 6 globaltimer stamps per work item (poll start, deps met, TMA issued,
+ * data landed, computed, published) copied into host `out` (capacity `cap`
+ * stamps); *n = item count */
+int fasmg_engine_wave_trace(void* engine, int level, unsigned long long* out, long cap, long* n);
 
 /* ---- axis-0 slab decomposition -------------------
  * One engine per rank owns the slab `rank` of every level whose block-plane

@@ -35,6 +35,8 @@
 //  * outer residual + sum of squares fused (no residual array).
 // The whole V-cycle plus the residual norm is captured once as a CUDA
 // graph and replayed per outer iteration.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -95,6 +97,7 @@ __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
 }
 
 #include "fasmg_stencil.cuh"
+#include "fasmg_wave.cuh"
 
 // ------------------------------------------------- edge-centered transfers
 // Reader of raw stored values at core (grid) index x in the blocked layout.
@@ -484,8 +487,9 @@ struct Engine {
     long kernels_per_vcycle = 0;
     long kernels_per_vcycle_norm = 0;
     // 0: thread per block, 1: per (block, class), 2: 2.5D register march,
-    // 3: 2.5D shared-memory march for large 3D levels (default), else 0
-    int sweep_variant = 3;
+    // 3: 2.5D shared-memory march (cp.async) for large 3D levels, 4: the
+    // same march fed by TMA boxes (default), else 0
+    int sweep_variant = 4;
     int march_chunk = 0;    // planes per marching chunk (0: per-level default)
     int sweep_minb = 3;     // min resident CTAs of the 3D half-sweep (register cap)
     // ---- axis-0 slab decomposition (multi-GPU / virtual ranks) ----
@@ -502,6 +506,16 @@ struct Engine {
     };
     std::vector<Peer> peers;            // size nranks once connected
     bool sharded(int k) const { return nranks > 1 && k < kg; }
+    // ---- temporally blocked smoothing (fasmg_wave.cuh) ----
+    int wave_T = 0;                     // FASMG_WAVE_T: half-sweeps per launch (0: off)
+    int wave_lag = 2;                   // FASMG_WAVE_LAG: ticket-order lag (1 or 2)
+    int wave_K = 4;                     // FASMG_WAVE_K: tiles per ticket
+    long wave_min = 1L << 18;           // FASMG_WAVE_MIN: min interior blocks of a level
+    int wave_grid = 0;                  // resident CTAs (occupancy x SMs)
+    unsigned* wave_buf = nullptr;       // ticket + [T][B0+2] completion counters
+    bool wave_ok[32] = {};
+    bool tma_ok[32] = {};               // level k half-sweeps use k_sweep_tma
+    CUtensorMap mapH[32], mapI[32], mapF[32], mapT[32];
 };
 
 struct Tile {
@@ -581,7 +595,22 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         k_sweep_march<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
         return;
     }
-    if (D == 3 && E.sweep_variant == 3 && __builtin_popcount(M) > 1 && L.B[2] >= 32 &&
+    if (D == 3 && E.sweep_variant == 4 && E.tma_ok[k] && __builtin_popcount(M) > 1) {
+        using namespace tsw;
+        const long tiles = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
+        int chunk = E.march_chunk;
+        if (chunk <= 0) {
+            chunk = 4;
+            for (int c = 16; c >= 8; c >>= 1)
+                if (tiles * ((L.B[0] + c - 1) / c) >= 1184) { chunk = c; break; }
+        }
+        dim3 blk(TX, TY, 1);
+        dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
+        k_sweep_tma<EA, M><<<grd, blk, SMEM, E.stream>>>(E.mapT[k], E.mapF[k], E.P[k], L, E.bc,
+                                                         chunk);
+        return;
+    }
+    if (D == 3 && E.sweep_variant >= 3 && __builtin_popcount(M) > 1 && L.B[2] >= 32 &&
         L.B[1] >= 8 && L.nblk >= (1L << 21)) {
         using namespace smem_sweep;
         // planes per marching chunk: long chunks amortize the two window
@@ -735,8 +764,56 @@ static void gather_level(Engine& E, int k, long& cnt) {
     launch_pad_fill<D>(E, k, cnt);
 }
 
+// T half-sweeps (seq[i0 .. i0+T)) of level k in one wavefront launch
+static void launch_wave(Engine& E, int k, const std::vector<unsigned>& seq, int i0, int T,
+                        long& cnt, unsigned long long* trace = nullptr) {
+    const Lvl& L = E.L[k];
+    WaveArgs A;
+    A.P = E.P[k];
+    A.T = T;
+    A.odd = 0;
+    for (int t = 0; t < T; ++t)
+        if (seq[i0 + t] == 0x96u) A.odd |= 1u << t;
+    A.ntx = L.B[2] / wave::TX;
+    A.nty = L.B[1] / wave::TY;
+    A.K = std::max(1, E.wave_K);
+    A.K = std::min(A.K, A.ntx);
+    A.gpr = (A.ntx + A.K - 1) / A.K;
+    A.ng = A.gpr * A.nty;
+    A.ticket = E.wave_buf;
+    A.flags = E.wave_buf + 32;  // keep the hot ticket on its own line
+    A.lag = E.wave_lag;
+    A.cyc1 = E.bc.kind[1][0] == BC_PERIODIC ? 1 : 0;
+    A.trace = trace;
+    A.ngroups = (long long)(L.B[0] + A.lag * (T - 1)) * T * A.ng;
+    cudaMemsetAsync(E.wave_buf, 0, sizeof(unsigned) * (32 + (size_t)T * (L.B[0] + 2) * A.nty),
+                    E.stream);
+    const int grid = (int)std::min<long long>(E.wave_grid, A.ngroups);
+    EA_DISPATCH(3, E.ea, (k_smooth_wave<EA><<<grid, wave::NTHR, wave::SMEM, E.stream>>>(
+                             E.mapH[k], E.mapI[k], E.mapF[k], L, E.bc, A)));
+    ++cnt;
+}
+
+// can the smoothing sequence of level k run as wavefront launches?
+static bool wave_seq(const Engine& E, int k, std::vector<unsigned>& seq) {
+    if (!E.wave_ok[k] || E.wave_T <= 0) return false;
+    seq.clear();
+    for (int it = 0; it < E.s; ++it)
+        for (unsigned m : E.masks) {
+            if (m != 0x96u && m != 0x69u) return false;
+            seq.push_back(m);
+        }
+    return true;
+}
+
 template <int D>
 static void launch_smooth(Engine& E, int k, long& cnt) {
+    std::vector<unsigned> seq;
+    if (D == 3 && wave_seq(E, k, seq)) {
+        const int n = (int)seq.size();
+        for (int i = 0; i < n; i += E.wave_T) launch_wave(E, k, seq, i, std::min(E.wave_T, n - i), cnt);
+        return;
+    }
     const Tile t = tile_of(E.L[k]);
     for (int it = 0; it < E.s; ++it)
         for (unsigned m : E.masks) {
@@ -849,6 +926,97 @@ static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* e
     if (with_norm) E.kernels_per_vcycle_norm = cnt;
     else E.kernels_per_vcycle = cnt;
     return 0;
+}
+
+// Tensor maps of a level's blocked array as a 4D tensor (pitch, E1, E0,
+// class) for TMA boxes.
+static bool encode_map(CUtensorMap* m, double* base, const Lvl& L, unsigned bx, unsigned by) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    cuuint64_t dims[4] = {(cuuint64_t)L.s1, (cuuint64_t)L.E[1], (cuuint64_t)L.E[0], 8};
+    cuuint64_t strides[3] = {(cuuint64_t)L.s1 * 8, (cuuint64_t)L.s0 * 8, (cuuint64_t)L.cls * 8};
+    cuuint32_t box[4] = {bx, by, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Decide which levels smooth by wavefront launches and prepare them.
+template <int EA>
+static int wave_attr(int* occ) {
+    cudaError_t e = cudaFuncSetAttribute(k_smooth_wave<EA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)wave::SMEM);
+    if (e != cudaSuccess) return fasmg_check(e);
+    return fasmg_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_smooth_wave<EA>,
+                                                                     wave::NTHR, wave::SMEM));
+}
+
+template <int EA>
+static int tma_attr() {
+    const int sm = (int)tsw::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_tma<EA, 0x96u>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep_tma<EA, 0x69u>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return fasmg_check(e);
+}
+
+// TMA maps of the levels whose half-sweeps run k_sweep_tma
+static int tma_setup(Engine& E) {
+    if (E.dim != 3 || E.sweep_variant != 4) return 0;
+    long min_blocks = 1L << 21;  // FASMG_TMA_MIN: smaller levels are launch-latency bound
+    if (const char* v = getenv("FASMG_TMA_MIN")) min_blocks = atol(v);
+    bool any = false;
+    for (int k = 0; k < E.nl; ++k) {
+        const Lvl& L = E.L[k];
+        if (L.B[2] < 32 || L.B[1] < 8 || L.nblk < min_blocks) continue;
+        E.tma_ok[k] = encode_map(&E.mapT[k], E.P[k], L, tsw::HX, tsw::HY) &&
+                      encode_map(&E.mapF[k], E.F[k], L, tsw::TX, tsw::TY);
+        any = any || E.tma_ok[k];
+    }
+    if (!any) return 0;
+    int st = 0;
+    EA_DISPATCH(3, E.ea, (st = tma_attr<EA>()));
+    return st;
+}
+
+static int wave_setup(Engine& E) {
+    if (int st = tma_setup(E)) return st;
+    if (const char* v = getenv("FASMG_WAVE_T")) E.wave_T = std::max(0, std::min(32, atoi(v)));
+    if (const char* v = getenv("FASMG_WAVE_K")) E.wave_K = std::max(1, atoi(v));
+    if (const char* v = getenv("FASMG_WAVE_LAG")) E.wave_lag = std::max(1, std::min(4, atoi(v)));
+    if (const char* v = getenv("FASMG_WAVE_MIN")) E.wave_min = atol(v);
+    if (E.dim != 3 || E.wave_T <= 0 || E.sweep_variant < 3) return 0;
+    if (E.bc.kind[0][0] == BC_PERIODIC || E.bc.kind[0][1] == BC_PERIODIC) return 0;
+    long maxp = 0;
+    for (int k = 0; k < E.nl; ++k) {
+        const Lvl& L = E.L[k];
+        if (E.sharded(k) || L.nblk < E.wave_min || L.B[2] % wave::TX || L.B[1] % wave::TY) continue;
+        E.wave_ok[k] = encode_map(&E.mapH[k], E.P[k], L, wave::HX, wave::HY) &&
+                       encode_map(&E.mapI[k], E.P[k], L, wave::TX, wave::TY) &&
+                       encode_map(&E.mapF[k], E.F[k], L, wave::TX, wave::TY);
+        if (E.wave_ok[k]) maxp = std::max(maxp, ((long)L.B[0] + 2) * (L.B[1] / wave::TY));
+    }
+    if (!maxp) return 0;
+    int occ = 0, dev = 0, sms = 0;
+    int st = 0;
+    EA_DISPATCH(3, E.ea, (st = wave_attr<EA>(&occ)));
+    if (st) return st;
+    if ((st = fasmg_check(cudaGetDevice(&dev)))) return st;
+    if ((st = fasmg_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)))) return st;
+    E.wave_grid = std::max(1, occ) * sms;
+    const size_t bytes = sizeof(unsigned) * (32 + (size_t)E.wave_T * maxp);
+    if ((st = fasmg_check(cudaMalloc(&E.wave_buf, bytes)))) return st;
+    return fasmg_check(cudaMemsetAsync(E.wave_buf, 0, bytes, E.stream));
 }
 
 static Lvl make_lvl(int dim, const int* n, int ea, double dmin, double dmax, double a,
@@ -993,6 +1161,7 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         }
         for (int t = 0; t < dim; ++t) nn[t] /= 2;
     }
+    if (int st = wave_setup(*E)) { delete E; fasmg_set_error(st, "wave setup failed"); return nullptr; }
     E->npart = (int)tile_ctas(tile_of(E->L[0]));
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
@@ -1114,6 +1283,7 @@ void fasmg_engine_destroy(void* h) {
     cudaFree(E->flags);
     cudaFree(E->cnt);
     cudaFree(E->allpart);
+    if (E->wave_buf) cudaFree(E->wave_buf);
     delete E;
 }
 
@@ -1275,6 +1445,32 @@ int fasmg_engine_time_sweeps(void* h, int k, int reps, double* ms) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     return st ? st : fasmg_check_launch();
+}
+
+// Debug: run the first wavefront launch of level k's smoothing stage with a
+// trace buffer of 6 globaltimer stamps per item (t, b0, tile) and copy it to
+// host memory `out` (size 6*T*B0*ntiles).  Returns the item count in *n.
+int fasmg_engine_wave_trace(void* h, int k, unsigned long long* out, long cap, long* n) {
+    Engine* E = (Engine*)h;
+    std::vector<unsigned> seq;
+    if (E->dim != 3 || k < 0 || k >= E->nl || !wave_seq(*E, k, seq))
+        return fasmg_set_error(FASMG_EINVAL, "level does not use wavefront smoothing");
+    const Lvl& L = E->L[k];
+    const int T = std::min(E->wave_T, (int)seq.size());
+    const long items = (long)T * L.B[0] * (L.B[2] / wave::TX) * (L.B[1] / wave::TY);
+    *n = items;
+    if (cap < 6 * items) return fasmg_set_error(FASMG_EINVAL, "trace buffer too small");
+    unsigned long long* d = nullptr;
+    int st = fasmg_check(cudaMalloc(&d, sizeof(unsigned long long) * 6 * items));
+    if (st) return st;
+    cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 6 * items, E->stream);
+    long cnt = 0;
+    launch_wave(*E, k, seq, 0, T, cnt, d);
+    st = fasmg_check(cudaMemcpyAsync(out, d, sizeof(unsigned long long) * 6 * items,
+                                     cudaMemcpyDeviceToHost, E->stream));
+    if (!st) st = fasmg_check(cudaStreamSynchronize(E->stream));
+    cudaFree(d);
+    return st;
 }
 
 // kernels launched per V-cycle (with_norm: V-cycle + outer residual norm),

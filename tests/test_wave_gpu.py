@@ -1,0 +1,136 @@
+"""Temporally blocked (wavefront) smoothing launches (csrc/fasmg_wave.cuh):
+bitwise parity with the CPU oracle and with the per-half-sweep path, for
+every cell/edge location, boundary kinds on every axis the wavefront
+supports, and several launch splittings (T half-sweeps per launch, K tiles
+per ticket).  The wavefront is forced onto small levels with
+FASMG_WAVE_MIN=0 so that the oracle finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import cases as C  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+HIST_RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_11152_b200 as pkg
+    return pkg
+
+
+LOC = {"cell": "CELL", "edge_ew": "EDGE_EW", "edge_ns": "EDGE_NS", "edge_tb": "EDGE_TB"}
+
+FACES = {
+    "dirichlet": None,
+    "lid": None,
+    # y periodic (in-plane wrap), x / z mixed Dirichlet values and Neumann
+    "mixed_yz": {"xlo": ("dirichlet", 0.25), "xhi": ("neumann", 0.0),
+                 "ylo": ("periodic", 0.0), "yhi": ("periodic", 0.0),
+                 "zlo": ("neumann", 0.0), "zhi": ("dirichlet", -1.0)},
+    "neumann_x": {"xlo": ("neumann", 0.0), "xhi": ("neumann", 0.0),
+                  "ylo": ("dirichlet", 0.0), "yhi": ("dirichlet", 1.0),
+                  "zlo": ("periodic", 0.0), "zhi": ("periodic", 0.0)},
+}
+
+
+def faces_of(spec):
+    f = FACES[spec]
+    return C.bc_faces(3, spec) if f is None else dict(f)
+
+
+def bc_of(P, faces):
+    return P.BoundaryCondition(3, tuple((nm, P.FaceRule(k, v)) for nm, (k, v) in faces.items()))
+
+
+def run_gpu(P, monkeypatch, env, shape, loc, faces, p0, f0, ml, k_max):
+    env = dict(env)
+    if "FASMG_WAVE_MIN" in env:
+        env.setdefault("FASMG_WAVE_T", 4)
+    for k, v in env.items():
+        monkeypatch.setenv(k, str(v))
+    if len(set(shape)) == 1:
+        g = P.unit_grid(shape)
+    else:  # uniform h on a box domain
+        g = P.GridLevel(0, shape, (0.0,) * 3, tuple(s / shape[-1] for s in shape))
+    L = getattr(P.Location, LOC[loc])
+    p = P.Field(g, L, 1, p0.copy())
+    f = P.Field(g, L, 1, f0.copy())
+    _, rep = P.solve(p, f, P.OperatorCoeffs(1.0, 0.5), P.FasParams(1e-30, k_max, 2, ml),
+                     P.make_plan("x", 3), bc_of(P, faces))
+    torch.cuda.synchronize()
+    return p.data.cpu().numpy(), rep
+
+
+@pytest.mark.parametrize("n,loc,spec,env", [
+    (64, "cell", "dirichlet", {"FASMG_WAVE_MIN": 0}),
+    (64, "cell", "dirichlet", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 3, "FASMG_WAVE_K": 1}),
+    (64, "cell", "dirichlet", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 1, "FASMG_WAVE_K": 7}),
+    (64, "cell", "mixed_yz", {"FASMG_WAVE_MIN": 0}),
+    (64, "cell", "neumann_x", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 5}),
+    (64, "edge_ew", "lid", {"FASMG_WAVE_MIN": 0}),
+    (64, "edge_ns", "mixed_yz", {"FASMG_WAVE_MIN": 0}),
+    (64, "edge_tb", "lid", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 4}),
+    (128, "cell", "dirichlet", {"FASMG_WAVE_T": 8, "FASMG_WAVE_LAG": 1}),
+])
+def test_wave_vs_oracle(P, monkeypatch, n, loc, spec, env):
+    import oracle as O
+    shape = (n,) * 3
+    ml = int(np.log2(n)) - 1
+    faces = faces_of(spec)
+    p0 = C.rand_field(21, shape, loc, 1)
+    f0 = C.rand_field(22, shape, loc, 1)
+    op = O.OField(shape, loc, 1, p0.copy())
+    of = O.OField(shape, loc, 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 2, 2, ml)
+    O.set_threads(1)
+    got, rep = run_gpu(P, monkeypatch, env, shape, loc, faces, p0, f0, ml, 2)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+
+
+def test_wave_matches_half_sweep_path(P, monkeypatch):
+    """Same engine inputs, wavefront on vs off: bitwise equal fields."""
+    shape = (128, 64, 64)
+    faces = faces_of("mixed_yz")
+    p0 = C.rand_field(31, shape, "cell", 1)
+    f0 = C.rand_field(32, shape, "cell", 1)
+    on, r1 = run_gpu(P, monkeypatch, {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 8}, shape, "cell",
+                     faces, p0, f0, 5, 3)
+    off, r2 = run_gpu(P, monkeypatch, {"FASMG_WAVE_T": 0}, shape, "cell", faces, p0, f0, 5, 3)
+    assert np.array_equal(on.view(np.uint64), off.view(np.uint64))
+    assert r1.residual_history == r2.residual_history
+
+
+@pytest.mark.parametrize("shape,loc,spec", [
+    ((64, 64, 64), "cell", "dirichlet"),
+    ((48, 112, 80), "cell", "mixed_yz"),      # partial tile along b2
+    ((64, 64, 96), "edge_ew", "lid"),
+    ((64, 48, 64), "edge_ns", "neumann_x"),
+    ((32, 64, 128), "edge_tb", "lid"),
+])
+def test_tma_sweep_vs_oracle(P, monkeypatch, shape, loc, spec):
+    """k_sweep_tma (TMA-fed marching half-sweep) forced onto small levels:
+    bitwise equal to the oracle, including partial edge tiles."""
+    import oracle as O
+    faces = faces_of(spec)
+    ml = 3
+    p0 = C.rand_field(41, shape, loc, 1)
+    f0 = C.rand_field(42, shape, loc, 1)
+    op = O.OField(shape, loc, 1, p0.copy())
+    of = O.OField(shape, loc, 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 2, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    got, rep = run_gpu(P, monkeypatch, {"FASMG_TMA_MIN": 0, "FASMG_MARCH_CHUNK": 3}, shape, loc,
+                       faces, p0, f0, ml, 2)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
