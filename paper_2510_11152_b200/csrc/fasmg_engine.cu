@@ -98,6 +98,7 @@ __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
 
 #include "fasmg_stencil.cuh"
 #include "fasmg_wave.cuh"
+#include "fasmg_coarse.cuh"
 
 // ------------------------------------------------- edge-centered transfers
 // Reader of raw stored values at core (grid) index x in the blocked layout.
@@ -516,6 +517,11 @@ struct Engine {
     bool wave_ok[32] = {};
     bool tma_ok[32] = {};               // level k half-sweeps use k_sweep_tma
     CUtensorMap mapH[32], mapI[32], mapF[32], mapT[32];
+    // ---- coarse levels in one cluster launch (fasmg_coarse.cuh) ----
+    int coarse_k0 = -1;                 // first level run by k_coarse_cycle (-1: none)
+    int coarse_cs = 8;                  // FASMG_COARSE_CS: CTAs per cluster
+    long coarse_max = 4096;             // FASMG_COARSE_MAX: max blocks of a coarse level
+    CoarseArgs* dcoarse = nullptr;      // device copy of the level table
 };
 
 struct Tile {
@@ -824,10 +830,33 @@ static void launch_smooth(Engine& E, int k, long& cnt) {
 }
 
 template <int D>
+static void launch_coarse(Engine& E, long& cnt) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(E.coarse_cs, 1, 1);
+    cfg.blockDim = dim3(512, 1, 1);
+    cfg.stream = E.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = E.coarse_cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_coarse_cycle<D>, (const CoarseArgs*)E.dcoarse);
+    ++cnt;
+}
+
+template <int D>
 static void launch_vcycle(Engine& E, long& cnt) {
     const unsigned ALL = (1u << (1 << D)) - 1;
+    // levels >= kc run inside one cluster launch
+    const int kc = E.coarse_k0 >= 0 ? E.coarse_k0 : E.nl;
+    if (kc == 0) {
+        launch_coarse<D>(E, cnt);
+        return;
+    }
     // descent
-    for (int k = 0; k < E.nl - 1; ++k) {
+    for (int k = 0; k < std::min(kc, E.nl - 1); ++k) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L), tc = tile_of(Lc);
@@ -857,9 +886,10 @@ static void launch_vcycle(Engine& E, long& cnt) {
         ++cnt;
         neighbor_barrier(E, k + 1, cnt);
     }
-    launch_smooth<D>(E, E.nl - 1, cnt);  // coarsest: s smoothing steps
+    if (kc < E.nl) launch_coarse<D>(E, cnt);
+    else launch_smooth<D>(E, E.nl - 1, cnt);  // coarsest: s smoothing steps
     // ascent
-    for (int k = E.nl - 2; k >= 0; --k) {
+    for (int k = std::min(kc, E.nl - 1) - 1; k >= 0; --k) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L);
@@ -989,7 +1019,41 @@ static int tma_setup(Engine& E) {
     return st;
 }
 
+// Levels from coarse_k0 down run in k_coarse_cycle: cell-centered, not
+// sharded, at most coarse_max blocks.
+static int coarse_setup(Engine& E) {
+    if (const char* v = getenv("FASMG_COARSE_MAX")) E.coarse_max = atol(v);
+    if (const char* v = getenv("FASMG_COARSE_CS")) E.coarse_cs = std::max(1, std::min(16, atoi(v)));
+    if (E.ea >= 0 || E.coarse_max <= 0 || E.masks.size() > 16) return 0;
+    int k0 = E.nl;
+    while (k0 > 0 && !E.sharded(k0 - 1) && E.L[k0 - 1].nblk <= E.coarse_max) --k0;
+    if (k0 >= E.nl) return 0;
+    CoarseArgs h;
+    memset(&h, 0, sizeof(h));
+    for (int k = 0; k < E.nl; ++k) {
+        h.P[k] = E.P[k];
+        h.F[k] = E.F[k];
+        h.L[k] = E.L[k];
+    }
+    h.bc = E.bc;
+    h.k0 = k0;
+    h.nl = E.nl;
+    h.s = E.s;
+    h.nm = (int)E.masks.size();
+    for (int j = 0; j < h.nm; ++j) h.masks[j] = E.masks[j];
+    int st = fasmg_check(cudaMalloc(&E.dcoarse, sizeof(CoarseArgs)));
+    if (!st) st = fasmg_check(cudaMemcpy(E.dcoarse, &h, sizeof(h), cudaMemcpyHostToDevice));
+    if (!st && E.coarse_cs > 8) {
+        st = fasmg_check(cudaFuncSetAttribute(E.dim == 3 ? (const void*)k_coarse_cycle<3>
+                                                         : (const void*)k_coarse_cycle<2>,
+                                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    if (!st) E.coarse_k0 = k0;
+    return st;
+}
+
 static int wave_setup(Engine& E) {
+    if (int st = coarse_setup(E)) return st;
     if (int st = tma_setup(E)) return st;
     if (const char* v = getenv("FASMG_WAVE_T")) E.wave_T = std::max(0, std::min(32, atoi(v)));
     if (const char* v = getenv("FASMG_WAVE_K")) E.wave_K = std::max(1, atoi(v));
@@ -1161,7 +1225,7 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         }
         for (int t = 0; t < dim; ++t) nn[t] /= 2;
     }
-    if (int st = wave_setup(*E)) { delete E; fasmg_set_error(st, "wave setup failed"); return nullptr; }
+    if (int st = wave_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (TMA maps, coarse cluster, wavefront) failed"); return nullptr; }
     E->npart = (int)tile_ctas(tile_of(E->L[0]));
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
@@ -1284,6 +1348,7 @@ void fasmg_engine_destroy(void* h) {
     cudaFree(E->cnt);
     cudaFree(E->allpart);
     if (E->wave_buf) cudaFree(E->wave_buf);
+    if (E->dcoarse) cudaFree(E->dcoarse);
     delete E;
 }
 

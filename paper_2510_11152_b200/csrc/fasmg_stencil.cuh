@@ -171,12 +171,9 @@ __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
 // ------------------------------------------------------------- smoothing
 // One launch = the reference's colors whose classes are in MASK (mutually
 // independent classes; PKG/smoothers.py:136-153).  Thread per block.
-template <int D, int EA, unsigned MASK, int MINB = 3>
-__global__ void __launch_bounds__(256, MINB) k_sweep_fast(double* __restrict__ P,
-                                                    const double* __restrict__ F, Lvl L,
-                                                    BcSpec bc) {
-    int bb[3];
-    if (!tile_coords<D>(L, bb)) return;
+template <int D, int EA, unsigned MASK>
+__device__ __forceinline__ void sweep_pt(double* __restrict__ P, const double* __restrict__ F,
+                                         const Lvl& L, const BcSpec& bc, const int* bb) {
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
     constexpr int NC = 1 << D;
     // phase 1: issue every load of every class before any arithmetic, so
@@ -224,6 +221,15 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_fast(double* __restrict__ P
         P[o] = nv[c];
         if (bnd) write_pads<D, EA>(P, L, bc, c, bb, o, nv[c]);
     }
+}
+
+template <int D, int EA, unsigned MASK, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) k_sweep_fast(double* __restrict__ P,
+                                                    const double* __restrict__ F, Lvl L,
+                                                    BcSpec bc) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    sweep_pt<D, EA, MASK>(P, F, L, bc, bb);
 }
 
 // Same update, one thread per (block, class): grid.z enumerates (b0, k-th
@@ -573,12 +579,10 @@ __device__ __forceinline__ void coarse_of(const Lvl& L, const Lvl& Lc, const int
 // coarse level's blocked arrays with its ghost pads (full BC on p_c,
 // PKG/fas.py:99-107).
 template <int D>
-__global__ void __launch_bounds__(256) k_tau_fast(const double* __restrict__ P,
-                                                  const double* __restrict__ F, Lvl L,
-                                                  double* __restrict__ Pc,
-                                                  double* __restrict__ Fc, Lvl Lc, BcSpec bc) {
-    int bb[3];
-    if (!tile_coords<D>(L, bb)) return;
+__device__ __forceinline__ void tau_pt(const double* __restrict__ P, const double* __restrict__ F,
+                                       const Lvl& L, double* __restrict__ Pc,
+                                       double* __restrict__ Fc, const Lvl& Lc, const BcSpec& bc,
+                                       const int* bb) {
     constexpr int NC = 1 << D;
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
     // phase 1: all loads (2^d centers, 2^d f, and the d*2^(d-1) neighbors
@@ -627,12 +631,21 @@ __global__ void __launch_bounds__(256) k_tau_fast(const double* __restrict__ P,
     if (on_boundary<D>(Lc, cb)) write_pads<D, -1>(Pc, Lc, bc, cc, cb, oc, pcv);
 }
 
-// f_c += a*p_c - b*Lap(p_c) on the coarse level (PKG/fas.py:108-110)
-template <int D, int EA>
-__global__ void __launch_bounds__(256) k_coarse_src_fast(const double* __restrict__ Pc,
-                                                         double* __restrict__ Fc, Lvl L) {
+template <int D>
+__global__ void __launch_bounds__(256) k_tau_fast(const double* __restrict__ P,
+                                                  const double* __restrict__ F, Lvl L,
+                                                  double* __restrict__ Pc,
+                                                  double* __restrict__ Fc, Lvl Lc, BcSpec bc) {
     int bb[3];
     if (!tile_coords<D>(L, bb)) return;
+    tau_pt<D>(P, F, L, Pc, Fc, Lc, bc, bb);
+}
+
+// f_c += a*p_c - b*Lap(p_c) on the coarse level (PKG/fas.py:108-110)
+template <int D, int EA>
+__device__ __forceinline__ void coarse_src_pt(const double* __restrict__ Pc,
+                                              double* __restrict__ Fc, const Lvl& L,
+                                              const int* bb) {
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
@@ -642,15 +655,21 @@ __global__ void __launch_bounds__(256) k_coarse_src_fast(const double* __restric
     }
 }
 
+template <int D, int EA>
+__global__ void __launch_bounds__(256) k_coarse_src_fast(const double* __restrict__ Pc,
+                                                         double* __restrict__ Fc, Lvl L) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    coarse_src_pt<D, EA>(Pc, Fc, L, bb);
+}
+
 // Cell-centered coarse correction (PKG/fas.py:119-123): c = p_c - R(p), R(p)
 // recomputed from the unchanged fine p (equals the reference's pinit),
 // injected and added; refreshes the fine ghost pads.
 template <int D>
-__global__ void __launch_bounds__(256) k_correct_fast(double* __restrict__ P, Lvl L,
-                                                      const double* __restrict__ Pc, Lvl Lc,
-                                                      BcSpec bc) {
-    int bb[3];
-    if (!tile_coords<D>(L, bb)) return;
+__device__ __forceinline__ void correct_pt(double* __restrict__ P, const Lvl& L,
+                                           const double* __restrict__ Pc, const Lvl& Lc,
+                                           const BcSpec& bc, const int* bb) {
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
     double pv[1 << D];
     double rp = 0.0;
@@ -671,6 +690,15 @@ __global__ void __launch_bounds__(256) k_correct_fast(double* __restrict__ P, Lv
         P[o] = v;
         if (bnd) write_pads<D, -1>(P, L, bc, c, bb, o, v);
     }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_correct_fast(double* __restrict__ P, Lvl L,
+                                                      const double* __restrict__ Pc, Lvl Lc,
+                                                      BcSpec bc) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    correct_pt<D>(P, L, Pc, Lc, bc, bb);
 }
 
 // residual into R (edge fields: input of the tangential restriction)
