@@ -89,7 +89,17 @@ class ProjectionStepper:
     device fields.  ``slots`` holds exactly the schedule's resident fields."""
 
     def __init__(self, grid: GridLevel, params: NSParams, bcs: dict | None = None,
-                 device=None):
+                 device=None, forcing=None):
+        """``forcing(component, t)``: optional body force (interior array of
+        the component's edge grid) added to the momentum source as
+        ``f += dt*F(t)``, with t = t^{n+1} (order 1, backward Euler) or
+        the trapezoidal (F(t^n) + F(t^{n+1}))/2 (order 2, Crank-Nicolson;
+        this reproduces PAPER.md Table 8 to 2-3 digits, ``forcing_rule =
+        "mid"`` uses F(t^{n+1/2})) -- used by the manufactured
+        temporal-convergence test; None for the cavity."""
+        self.forcing = forcing
+        self.forcing_rule = "trap"  # order 2: (F^n + F^{n+1})/2, or "mid" F(t^{n+1/2})
+        self.t = 0.0
         self.grid = grid
         self.params = params
         self.dim = grid.dim
@@ -193,8 +203,22 @@ class ProjectionStepper:
             lap = laplacian(un)
             elem(RHS2, f.interior, [un.interior, conv.interior, gp, lap], s0=dt,
                  s1=dt / (2.0 * self.params.re))
+        if self.forcing is not None:
+            if order == 1:
+                F = self._force(c, self.t + dt)
+            elif self.forcing_rule == "trap":  # (F(t^n) + F(t^{n+1}))/2
+                F = 0.5 * (self._force(c, self.t) + self._force(c, self.t + dt))
+            else:                              # F(t^{n+1/2})
+                F = self._force(c, self.t + 0.5 * dt)
+            elem(AXPY, f.interior, [f.interior, F], s0=-dt)  # f + dt*F
         f.ghosts_fresh = False
         return f
+
+    def _force(self, c: str, t: float) -> torch.Tensor:
+        F = self.forcing(c, t)
+        if not torch.is_tensor(F):
+            F = torch.as_tensor(np.ascontiguousarray(F), dtype=torch.float64)
+        return F.to(self.device)
 
     def pressure_poisson(self, tld: dict, guess: Field) -> SolveReport:
         """-dt*Lap(p~) = -div(u~), all-Neumann, zero mean (SPEC.md:451-458);
@@ -263,6 +287,7 @@ class ProjectionStepper:
         ren = dict(sched.rebind)
         self.held = {slot: ren.get(q, q) for slot, q in self.held.items()}
         self.step_count += 1
+        self.t = self.step_count * dt
         return rep
 
     def _bind(self, q: str, slot: str):
