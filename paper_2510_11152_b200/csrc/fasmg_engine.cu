@@ -316,6 +316,227 @@ __global__ void __launch_bounds__(TPB) k_correct_edge(double* __restrict__ P, Lv
     }
 }
 
+// ---------------------------------------------- fast edge-field transfers
+// The transfers above evaluate the reference's ghost chain per read.  The
+// fast path first materialises every ghost / corner a transfer reads into
+// the blocked array's pad slots (k_pad_all), or the correction c = p_c -
+// pinit with its homogenized ghosts into a scratch array (k_corr_edge), and
+// then reads raw values: same values, same arithmetic, no per-read chains.
+
+// grid index of (class c, block b) along axis a, and whether a transfer
+// may read it (cell axis 0..n+1, edge axis 0..n)
+template <int D>
+__device__ __forceinline__ bool grid_idx(const Lvl& L, int c, const int* b, int* x, bool* inner) {
+    bool in = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        x[a] = 2 * b[a] - qbit<D>(c, a);
+        const bool edge = a == L.ea;
+        const int hi = edge ? L.n[a] : L.n[a] + 1;
+        if (x[a] < 0 || x[a] > hi) return false;
+        in = in && x[a] >= 1 && x[a] <= (edge ? L.n[a] - 1 : L.n[a]);
+    }
+    *inner = in;
+    return true;
+}
+
+// Every pad slot (faces, edges, corners) of a level's blocked array set to
+// the value fill_ghosts gives it under bc (PKG/boundary.py:90-156).  Thread
+// per pad block position of one face (grid.y = face), all classes.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, BcSpec bc) {
+    const int face = blockIdx.y, a = face >> 1, side = face & 1;
+    int oth[2], no = 0;
+#pragma unroll
+    for (int t = 0; t < D; ++t)
+        if (t != a) oth[no++] = t;
+    const long n1 = L.E[oth[0]], n2 = D == 3 ? L.E[oth[1]] : 1;
+    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n1 * n2) return;
+    int b[3] = {0, 0, 0};
+    b[a] = side ? L.B[a] + 1 : 0;
+    if (D == 3) {
+        b[oth[1]] = (int)(t % n2);
+        b[oth[0]] = (int)(t / n2);
+    } else {
+        b[oth[0]] = (int)t;
+    }
+    AxisGeo ax[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        ax[q].m = q < D ? L.n[q] : 1;
+        ax[q].edge = (q == L.ea);
+    }
+    BlkReader<D> rd{P, L};
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        int x[3] = {0, 0, 0};
+        bool in;
+        if (!grid_idx<D>(L, c, b, x, &in) || in) continue;
+        const double v = ghost_value<D>(ax, bc, x[0], x[1], x[2], rd);
+        P[at<D>(L, c, b[0], b[1], b[2])] = v;
+    }
+}
+
+// restrict_edge on raw reads (pads of Fn filled by k_pad_all).  Thread per
+// coarse interior point I (natural order, last axis fastest): fine edge-
+// axis columns 2I-1 (class bit 1) and 2I (bit 0) of block I; tangential
+// rows 2J-1 (bit 1, block J), 2J (bit 0, block J), 2J+1 (bit 1, block J+1).
+// The edge axis is a template parameter so every class/offset is a
+// compile-time constant; the arithmetic is KER/numba_backend.py:304-342.
+template <int D, int EA>
+__global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __restrict__ Fn, Lvl L,
+                                                            double* __restrict__ Co, Lvl Lc) {
+    constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = D == 3 ? (P0 == 2 ? 1 : 2) : 0;
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    long m[3];
+    for (int a = 0; a < 3; ++a) m[a] = a < D ? (a == P0 ? Lc.n[a] - 1 : Lc.n[a]) : 1;
+    if (t >= m[0] * m[1] * m[2]) return;
+    int I[3];
+    if (D == 3) {
+        I[2] = 1 + (int)(t % m[2]);
+        long r = t / m[2];
+        I[1] = 1 + (int)(r % m[1]);
+        I[0] = 1 + (int)(r / m[1]);
+    } else {
+        I[2] = 0;
+        I[1] = 1 + (int)(t % m[1]);
+        I[0] = 1 + (int)(t / m[1]);
+    }
+    const long base = at<D>(L, 0, I[0], I[1], D == 3 ? I[2] : 0);
+    // fine value: edge offset de (0: 2I-1, 1: 2I), tangential dj/dk (0: 2J-1,
+    // 1: 2J, 2: 2J+1)
+    auto F = [&](int de, int dj, int dk) {
+        int c = 0;
+        long o = base;
+        c |= (de == 0 ? 1 : 0) << (D - 1 - P0);
+        c |= (dj == 1 ? 0 : 1) << (D - 1 - P1);
+        if (dj == 2) o += bstride<D>(L, P1);
+        if (D == 3) {
+            c |= (dk == 1 ? 0 : 1) << (D - 1 - P2);
+            if (dk == 2) o += bstride<D>(L, P2);
+        }
+        return Fn[o + (long)c * L.cls];
+    };
+    double res;
+    if (D == 2) {
+        const double t1 = ad(ad(F(0, 0, 0), ml(2.0, F(0, 1, 0))), F(0, 2, 0));
+        const double t2 = ad(ad(F(1, 0, 0), ml(2.0, F(1, 1, 0))), F(1, 2, 0));
+        res = ml(ad(t1, t2), 0.125);
+    } else {
+        double tang[2];
+#pragma unroll
+        for (int cI = 0; cI < 2; ++cI) {
+            double rows[3];
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr)
+                rows[rr] = ml(ad(ad(F(cI, rr, 0), ml(2.0, F(cI, rr, 1))), F(cI, rr, 2)), 0.25);
+            tang[cI] = ml(ad(ad(rows[0], ml(2.0, rows[1])), rows[2]), 0.25);
+        }
+        res = ml(ad(tang[0], tang[1]), 0.5);
+    }
+    int cc = 0, cb[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        cc |= (I[a] & 1) << (D - 1 - a);
+        cb[a] = (I[a] + 1) >> 1;
+    }
+    Co[at<D>(Lc, cc, cb[0], cb[1], cb[2])] = res;
+}
+
+// Corr = the value CorrReader + ghost chain give at every coarse position a
+// prolongation reads (interior: p_c - pinit; ghosts under the homogenized
+// bc).  Thread per storage element of the coarse level.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc,
+                                                   const double* __restrict__ PI, Lvl Lc,
+                                                   BcSpec bch, double* __restrict__ Corr) {
+    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= Lc.cls * (1L << D)) return;
+    const int c = (int)(t / Lc.cls);
+    long rem = t - (long)c * Lc.cls - OFF;
+    if (rem < 0) return;
+    int b[3] = {0, 0, 0};
+    if (D == 3) {
+        b[0] = (int)(rem / Lc.s0);
+        rem -= (long)b[0] * Lc.s0;
+        b[1] = (int)(rem / Lc.s1);
+        b[2] = (int)(rem - (long)b[1] * Lc.s1);
+        if (b[0] >= Lc.E[0] || b[2] >= Lc.E[2]) return;
+    } else {
+        b[0] = (int)(rem / Lc.s0);
+        b[1] = (int)(rem - (long)b[0] * Lc.s0);
+        if (b[0] >= Lc.E[0] || b[1] >= Lc.E[1]) return;
+    }
+    int x[3] = {0, 0, 0};
+    bool in;
+    if (!grid_idx<D>(Lc, c, b, x, &in)) return;
+    CorrReader<D> rd{Pc, PI, Lc};
+    double v;
+    if (in) {
+        v = rd(x[0], x[1], x[2]);
+    } else {
+        AxisGeo ax[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            ax[q].m = q < D ? Lc.n[q] : 1;
+            ax[q].edge = (q == Lc.ea);
+        }
+        v = ghost_value<D>(ax, bch, x[0], x[1], x[2], rd);
+    }
+    Corr[at<D>(Lc, c, b[0], b[1], b[2])] = v;
+}
+
+// prolong_edge of Corr added to the fine interior (raw reads).  All 2^d
+// fine points of block bb draw on the same 2 x 3 (x 3) coarse neighbourhood
+// (edge-axis lines b-1, b; tangential b-1..b+1), loaded once into
+// registers; with the edge axis a template parameter every index below is
+// a compile-time constant.  Per fine point with parity bits (qe, qj, qk) in
+// the permuted axes (edge axis first): tangential j = b, j+dj = b-1 (q=1)
+// or b+1 (q=0); edge-axis line b (qe=0) or the mean of lines b-1, b (qe=1)
+// -- KER/numpy_backend.py:194-224.
+template <int D, int EA>
+__global__ void __launch_bounds__(TPB) k_correct_edge_fast(double* __restrict__ P, Lvl L,
+                                                           const double* __restrict__ Corr,
+                                                           Lvl Lc) {
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= L.nblk) return;
+    int bb[3];
+    decode<D>(L, t, bb);
+    constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = D == 3 ? (P0 == 2 ? 1 : 2) : 0;
+    const int be = bb[P0], bj = bb[P1], bk = D == 3 ? bb[P2] : 0;
+    BlkReader<D> rd{Corr, Lc};
+    double cv[2][3][3];
+#pragma unroll
+    for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+            for (int dk = 0; dk < 3; ++dk) {
+                if (D == 2 && dk > 0) { cv[di][dj][dk] = 0.0; continue; }
+                int g[3] = {0, 0, 0};
+                g[P0] = be - 1 + di;
+                g[P1] = bj - 1 + dj;
+                if (D == 3) g[P2] = bk - 1 + dk;
+                cv[di][dj][dk] = rd(g[0], g[1], g[2]);
+            }
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        if (!interior<D>(L, c, bb)) continue;
+        const int qe = qbit<D>(c, P0), qj = qbit<D>(c, P1), qk = D == 3 ? qbit<D>(c, P2) : 0;
+        const int jd = qj ? 0 : 2, kd = qk ? 0 : 2;
+        auto line = [&](int i) {
+            if (D == 2) return ml(ad(ml(3.0, cv[i][1][0]), cv[i][jd][0]), 0.25);
+            const double t_near = ml(ad(ml(3.0, cv[i][1][1]), cv[i][jd][1]), 0.25);
+            const double t_far = ml(ad(ml(3.0, cv[i][1][kd]), cv[i][jd][kd]), 0.25);
+            return ml(ad(ml(3.0, t_near), t_far), 0.25);
+        };
+        const double v = qe ? ml(ad(line(0), line(1)), 0.5) : line(1);
+        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
+        P[o] = ad(P[o], v);
+    }
+}
+
 __global__ void k_final_sum(const double* __restrict__ part, int n, double* out) {
     __shared__ double sh[1024];
     double acc = 0.0;
@@ -493,6 +714,7 @@ struct Engine {
     int sweep_variant = 4;
     int march_chunk = 0;    // planes per marching chunk (0: per-level default)
     int sweep_minb = 3;     // min resident CTAs of the 3D half-sweep (register cap)
+    int edge_fast = 1;      // FASMG_EDGE_FAST: pad-materialised edge transfers (0: ghost chains)
     // ---- axis-0 slab decomposition (multi-GPU / virtual ranks) ----
     int nranks = 1, rank = 0;
     int kg = 0;                         // first replicated level (levels < kg are slabs)
@@ -689,6 +911,19 @@ static void launch_pad_fill(Engine& E, int k, long& cnt) {
     ++cnt;
 }
 
+template <int D>
+static void launch_pad_all(Engine& E, double* P, const Lvl& L, const BcSpec& bc, long& cnt) {
+    long face = 1;
+    for (int a = 0; a < D; ++a) {
+        long f = 1;
+        for (int t = 0; t < D; ++t)
+            if (t != a) f *= L.E[t];
+        face = std::max(face, f);
+    }
+    k_pad_all<D><<<dim3(nb(face, TPB), 2 * D), TPB, 0, E.stream>>>(P, L, bc);
+    ++cnt;
+}
+
 // ---- slab exchanges (no-ops on a single rank) ----
 template <int D>
 static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt) {
@@ -870,10 +1105,21 @@ static void launch_vcycle(Engine& E, long& cnt) {
                                      E.P[k], E.F[k], E.R[k], L)));
             long mc = 1;
             for (int a = 0; a < D; ++a) mc *= (a == E.ea ? Lc.n[a] - 1 : Lc.n[a]);
-            k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.bc, E.P[k + 1],
-                                                                  Lc);
-            k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.R[k], L, E.bch, E.F[k + 1],
-                                                                  Lc);
+            if (E.edge_fast) {
+                launch_pad_all<D>(E, E.P[k], L, E.bc, cnt);
+                launch_pad_all<D>(E, E.R[k], L, E.bch, cnt);
+                EA_DISPATCH(D, E.ea, (k_restrict_edge_fast<D, EA><<<nb(mc, TPB), TPB, 0,
+                                                                    E.stream>>>(E.P[k], L,
+                                                                                E.P[k + 1], Lc)));
+                EA_DISPATCH(D, E.ea, (k_restrict_edge_fast<D, EA><<<nb(mc, TPB), TPB, 0,
+                                                                    E.stream>>>(E.R[k], L,
+                                                                                E.F[k + 1], Lc)));
+            } else {
+                k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.bc,
+                                                                      E.P[k + 1], Lc);
+                k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.R[k], L, E.bch,
+                                                                      E.F[k + 1], Lc);
+            }
             long tot = Lc.cls * (1 << D);
             k_copy_blk<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], tot);
             cnt += 4;
@@ -897,9 +1143,19 @@ static void launch_vcycle(Engine& E, long& cnt) {
             k_correct_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc, E.bc);
             ++cnt;
         } else {
-            k_correct_edge<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1],
-                                                                     E.PI[k + 1], Lc, E.bch);
-            ++cnt;
+            if (E.edge_fast) {
+                const long tot = Lc.cls * (1L << D);
+                k_corr_edge<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc,
+                                                                   E.bch, E.R[k + 1]);
+                EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<nb(L.nblk, TPB), TPB, 0,
+                                                                   E.stream>>>(E.P[k], L,
+                                                                               E.R[k + 1], Lc)));
+                cnt += 2;
+            } else {
+                k_correct_edge<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1],
+                                                                         E.PI[k + 1], Lc, E.bch);
+                ++cnt;
+            }
             launch_pad_fill<D>(E, k, cnt);
         }
         halo_exchange<D>(E, k, ALL, cnt);
@@ -1182,6 +1438,7 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
     if (const char* v = getenv("FASMG_MARCH_CHUNK")) E->march_chunk = std::max(0, atoi(v));
     if (const char* v = getenv("FASMG_TILE_Y")) g_tile_y = std::max(1, atoi(v));
     if (const char* v = getenv("FASMG_SWEEP_MINB")) E->sweep_minb = atoi(v);
+    if (const char* v = getenv("FASMG_EDGE_FAST")) E->edge_fast = atoi(v);
     // sharded levels: a prefix of the hierarchy, never the coarsest
     E->kg = 0;
     if (nranks > 1) {
@@ -1218,9 +1475,9 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         cudaMemsetAsync(E->P[k], 0, bytes, E->stream);
         cudaMemsetAsync(E->F[k], 0, bytes, E->stream);
         if (ea >= 0) {
-            if (k < E->nl - 1 && fasmg_check(cudaMalloc(&E->R[k], bytes))) { delete E; return nullptr; }
+            if (fasmg_check(cudaMalloc(&E->R[k], bytes))) { delete E; return nullptr; }
             if (k >= 1 && fasmg_check(cudaMalloc(&E->PI[k], bytes))) { delete E; return nullptr; }
-            if (k < E->nl - 1) cudaMemsetAsync(E->R[k], 0, bytes, E->stream);
+            cudaMemsetAsync(E->R[k], 0, bytes, E->stream);
             if (k >= 1) cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
         }
         for (int t = 0; t < dim; ++t) nn[t] /= 2;

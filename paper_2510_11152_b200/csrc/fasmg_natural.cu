@@ -256,11 +256,17 @@ __device__ __forceinline__ double weno_point(double dm2, double dm1, double dp1,
     return ml(dv(ad(ml(a0, c0), ml(a1, c1)), ad(a0, a1)), inv_2h);
 }
 
+// The reference runs these axis-0 kernels on moveaxis views, so the view's
+// last axis may be the strided one; `fast` names the view axis with the
+// smallest output stride, which consecutive threads walk (coalescing only:
+// every point's arithmetic is unchanged).
 __global__ void k_weno2(double* out, S3 os, const double* q, S3 qs, const double* wind, S3 ws,
-                        int ni, int nj, int oi, int oj, double inv_2h, double eps) {
+                        int ni, int nj, int oi, int oj, double inv_2h, double eps, int fast) {
     long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (t >= (long)ni * nj) return;
-    int ii = (int)(t / nj), jj = (int)(t % nj);
+    int ii, jj;
+    if (fast == 1) { ii = (int)(t / nj); jj = (int)(t % nj); }
+    else { jj = (int)(t / ni); ii = (int)(t % ni); }
     int i = ii + oi, j = jj + oj;
     double dm2 = sb(q[I2(qs.s, i - 1, j)], q[I2(qs.s, i - 2, j)]);
     double dm1 = sb(q[I2(qs.s, i, j)], q[I2(qs.s, i - 1, j)]);
@@ -273,12 +279,17 @@ __global__ void k_weno2(double* out, S3 os, const double* q, S3 qs, const double
 
 __global__ void k_weno3(double* out, S3 os, const double* q, S3 qs, const double* wind, S3 ws,
                         int ni, int nj, int nk, int oi, int oj, int ok, double inv_2h,
-                        double eps) {
+                        double eps, int p0, int p1, int p2) {
     long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (t >= (long)ni * nj * nk) return;
-    int kk = (int)(t % nk);
-    long r = t / nk;
-    int jj = (int)(r % nj), ii = (int)(r / nj);
+    // view axes in order slowest (p0) .. fastest (p2)
+    const int d[3] = {ni, nj, nk};
+    int idx[3];
+    idx[p2] = (int)(t % d[p2]);
+    long r = t / d[p2];
+    idx[p1] = (int)(r % d[p1]);
+    idx[p0] = (int)(r / d[p1]);
+    const int ii = idx[0], jj = idx[1], kk = idx[2];
     int i = ii + oi, j = jj + oj, k = kk + ok;
     double dm2 = sb(q[I3(qs.s, i - 1, j, k)], q[I3(qs.s, i - 2, j, k)]);
     double dm1 = sb(q[I3(qs.s, i, j, k)], q[I3(qs.s, i - 1, j, k)]);
@@ -432,10 +443,54 @@ __global__ void k_chunk_sums(const double* v, S3 vs, int dim, int e0, int e1, in
     sums[c] = pw_sum(buf, len);
 }
 
+// Same per-chunk sums for chunks of exactly 128*2^k (k <= 6) elements --
+// the common case (B = 8192 whenever the trailing extents divide 8192):
+// numpy's split tree is then a perfect binary tree of 128-element leaves,
+// so one CTA gathers the chunk into shared memory (coalesced), 2^k threads
+// evaluate the leaves (pw_leaf) and a fixed pairwise tree combines them in
+// the recursion's order -- bitwise equal to pw_sum.
+constexpr int CH_LEAF = 128, CH_PAD = 129, CH_MAXLEAVES = 64;
+__global__ void __launch_bounds__(256) k_chunk_sums_tree(const double* v, S3 vs, int dim, int e0,
+                                                         int e1, int e2, long B, int nleaves,
+                                                         double* sums) {
+    extern __shared__ double sh[];  // [nleaves][CH_PAD] + [nleaves]
+    const long c = blockIdx.x;
+    const long start = c * B;
+    for (long t = threadIdx.x; t < B; t += blockDim.x) {
+        const long q = start + t;
+        long off;
+        if (dim == 2) {
+            off = (q / e1) * vs.s[0] + (q % e1) * vs.s[1];
+        } else {
+            long k = q % e2, r = q / e2;
+            off = (r / e1) * vs.s[0] + (r % e1) * vs.s[1] + k * vs.s[2];
+        }
+        sh[(t / CH_LEAF) * CH_PAD + (t % CH_LEAF)] = v[off];
+    }
+    __syncthreads();
+    double* leaf = sh + (long)nleaves * CH_PAD;
+    if ((int)threadIdx.x < nleaves) leaf[threadIdx.x] = pw_leaf(sh + threadIdx.x * CH_PAD, CH_LEAF);
+    __syncthreads();
+    for (int w = 1; w < nleaves; w <<= 1) {
+        const int i = threadIdx.x * 2 * w;
+        if (i + w < nleaves) leaf[i] = ad(leaf[i], leaf[i + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[c] = leaf[0];
+}
+
 __global__ void k_chunk_total(const double* sums, long nchunks, double* out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double acc = 0.0;
-    for (long c = 0; c < nchunks; ++c) acc = ad(acc, sums[c]);
+    long c = 0;
+    for (; c + 8 <= nchunks; c += 8) {  // loads issued ahead of the serial adds
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = sums[c + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = ad(acc, x[j]);
+    }
+    for (; c < nchunks; ++c) acc = ad(acc, sums[c]);
     out[0] = acc;
 }
 
@@ -735,18 +790,23 @@ int fasmg_weno_deriv0_2d(double* out, const long* os, const double* q, const lon
                          const double* wind, const long* ws, int ni, int nj, int oi, int oj,
                          double inv_2h, double eps, void* stream) {
     long n = (long)ni * nj;
+    const int fast = labs(os[0]) < labs(os[1]) ? 0 : 1;
     LAUNCH(n, (k_weno2<<<nblk(n, TPB), TPB, 0, S(stream)>>>(out, mk(os), q, mk(qs), wind,
                                                             mk(ws), ni, nj, oi, oj, inv_2h,
-                                                            eps)));
+                                                            eps, fast)));
 }
 
 int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const long* qs,
                          const double* wind, const long* ws, int ni, int nj, int nk, int oi,
                          int oj, int ok, double inv_2h, double eps, void* stream) {
     long n = (long)ni * nj * nk;
+    int p[3] = {0, 1, 2};  // sort view axes by output stride, largest first
+    for (int a = 0; a < 3; ++a)
+        for (int b = a + 1; b < 3; ++b)
+            if (labs(os[p[b]]) > labs(os[p[a]])) std::swap(p[a], p[b]);
     LAUNCH(n, (k_weno3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(out, mk(os), q, mk(qs), wind,
                                                             mk(ws), ni, nj, nk, oi, oj, ok,
-                                                            inv_2h, eps)));
+                                                            inv_2h, eps, p[0], p[1], p[2])));
 }
 
 // fill_ghosts on a natural-layout C-contiguous data array (PKG/boundary.py:90)
@@ -809,10 +869,26 @@ int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, dou
     long nch = (n + B - 1) / B;
     S3 s = mk(vs);
     if (dim == 2) s.s[2] = 0;
-    if (nch > 0)
+    int nleaves = 0;  // B = 128 * 2^k, k <= 6, and no partial last chunk
+    if (n % B == 0 && B % CH_LEAF == 0) {
+        long l = B / CH_LEAF;
+        if (l <= CH_MAXLEAVES && (l & (l - 1)) == 0) nleaves = (int)l;
+    }
+    if (nch > 0 && nleaves > 0) {
+        const size_t shm = sizeof(double) * ((size_t)nleaves * CH_PAD + nleaves);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_chunk_sums_tree, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double) * (CH_MAXLEAVES * CH_PAD + CH_MAXLEAVES)));
+            attr = true;
+        }
+        k_chunk_sums_tree<<<(unsigned)nch, 256, shm, S(stream)>>>(
+            v, s, dim, ext[0], ext[1], dim == 3 ? ext[2] : 1, B, nleaves, sums);
+    } else if (nch > 0) {
         k_chunk_sums<<<nblk(nch, 64), 64, 0, S(stream)>>>(v, s, dim, ext[0], ext[1],
                                                           dim == 3 ? ext[2] : 1, n, B, scratch,
                                                           sums, nch);
+    }
     k_chunk_total<<<1, 32, 0, S(stream)>>>(sums, nch, out);
     return fasmg_check_launch();
 }

@@ -198,3 +198,17 @@ def test_solver_vs_oracle_larger(P, n, dim, loc, bc):
                      P.make_plan("x", dim), bc_of(P, dim, bc))
     np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
     assert np.array_equal(host(p.data).view(np.uint64), op.data.view(np.uint64))
+
+
+@pytest.mark.parametrize("shape", [(34, 34, 34), (66, 130, 18), (10, 10, 10), (130, 258), (7, 9, 11),
+                                   (1026, 34)])
+def test_view_sum_tree_and_serial_paths(P, shape):
+    """Ordered (numpy 2.3 buffered-pairwise) interior sum on the device vs the
+    oracle restatement, for chunk lengths that take the parallel-tree path
+    (128*2^k) and ones that take the serial path."""
+    import oracle as O
+    from paper_2510_11152_b200.grid import view_sum
+    a = np.random.default_rng(sum(shape)).standard_normal(shape)
+    inner = tuple(slice(1, s - 1) for s in shape)
+    got = float(view_sum(dev(a)[inner]).item())
+    assert got == float(O.view_sum(a[inner]))

@@ -62,3 +62,26 @@ def test_divergence_free_after_projection(P):
     for _ in range(5):
         st.step()
         assert abs(st.divergence()) <= 1e-12
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_ns_3d_32_matches_oracle(P, order):
+    """Medium-size 3D cavity (32^3, mesh level 4): momentum and pressure
+    residual histories within 1e-10 and bitwise fields after 2 steps."""
+    import ns_oracle as NO
+    import oracle as O
+    st = _stepper(P, (32, 32, 32), order, "efficient", dt=1e-3)
+    O.set_threads(8)
+    orc = NO.NSOracle((32, 32, 32), 100.0, 1e-3, order)
+    try:
+        for k in range(2):
+            rep = st.step()
+            hist = orc.step()
+            for c in st.comps:
+                np.testing.assert_allclose(rep.momentum[c].residual_history, hist[c], rtol=1e-10)
+            np.testing.assert_allclose(rep.pressure.residual_history, hist["p"], rtol=1e-10)
+            for c in st.comps:
+                got = st.velocity(c).numpy()
+                assert np.array_equal(got.view(np.uint64), orc.un[c].data.view(np.uint64)), (k, c)
+    finally:
+        O.set_threads(1)
