@@ -22,7 +22,7 @@ struct CoarseArgs {
     double* F[32];
     Lvl L[32];
     BcSpec bc;
-    int k0, nl, s, nm;
+    int k0, k1, nl, s, nm;  // cluster levels k0..k1-1, CTA-0 levels k1..nl-1
     unsigned masks[16];
 };
 
@@ -71,13 +71,18 @@ __device__ __forceinline__ void sweep_dispatch(unsigned m, double* P, const doub
     }
 }
 
-template <int D>
-__global__ void __launch_bounds__(512) k_coarse_cycle(const CoarseArgs* __restrict__ A) {
-    const long gtid = (long)cluster_rank() * blockDim.x + threadIdx.x;
-    const long gstr = (long)cluster_size() * blockDim.x;
+// Sub-V-cycle over levels ka..nl-1 (descent from ka, coarsest smoothing,
+// ascent back to ka), by `gstr` threads with index `gtid`; CL selects the
+// barrier between dependent phases: the whole cluster (CL) or this CTA.
+template <int D, bool CL>
+__device__ __forceinline__ void run_levels(const CoarseArgs* __restrict__ A, int ka, int kb,
+                                           bool coarsest, long gtid, long gstr) {
     const BcSpec bc = A->bc;
-    const int k0 = A->k0, nl = A->nl;
-
+    const int nl = A->nl;
+    auto sync = [] {
+        if (CL) cluster_sync_all();
+        else __syncthreads();
+    };
     auto smooth = [&](int k) {
         const Lvl L = A->L[k];
         double* P = A->P[k];
@@ -90,11 +95,11 @@ __global__ void __launch_bounds__(512) k_coarse_cycle(const CoarseArgs* __restri
                     decode<D>(L, t, bb);
                     sweep_dispatch<D>(m, P, F, L, bc, bb);
                 }
-                cluster_sync_all();
+                sync();
             }
     };
-
-    for (int k = k0; k < nl - 1; ++k) {  // descent (PKG/fas.py:98-110)
+    // descent over ka..kb-1 (PKG/fas.py:98-110)
+    for (int k = ka; k < kb; ++k) {
         smooth(k);
         const Lvl L = A->L[k], Lc = A->L[k + 1];
         for (long t = gtid; t < L.nblk; t += gstr) {
@@ -102,23 +107,64 @@ __global__ void __launch_bounds__(512) k_coarse_cycle(const CoarseArgs* __restri
             decode<D>(L, t, bb);
             tau_pt<D>(A->P[k], A->F[k], L, A->P[k + 1], A->F[k + 1], Lc, bc, bb);
         }
-        cluster_sync_all();
+        sync();
         for (long t = gtid; t < Lc.nblk; t += gstr) {
             int bb[3];
             decode<D>(Lc, t, bb);
             coarse_src_pt<D, -1>(A->P[k + 1], A->F[k + 1], Lc, bb);
         }
-        cluster_sync_all();
+        sync();
     }
-    smooth(nl - 1);  // coarsest (PKG/fas.py:111-113)
-    for (int k = nl - 2; k >= k0; --k) {  // ascent (PKG/fas.py:115-124)
+    if (coarsest) smooth(nl - 1);  // PKG/fas.py:111-113
+    (void)nl;
+}
+
+template <int D, bool CL>
+__device__ __forceinline__ void run_ascent(const CoarseArgs* __restrict__ A, int ka, int kb,
+                                           long gtid, long gstr) {
+    const BcSpec bc = A->bc;
+    auto sync = [] {
+        if (CL) cluster_sync_all();
+        else __syncthreads();
+    };
+    // ascent over kb-1..ka (PKG/fas.py:115-124)
+    for (int k = kb - 1; k >= ka; --k) {
         const Lvl L = A->L[k], Lc = A->L[k + 1];
         for (long t = gtid; t < L.nblk; t += gstr) {
             int bb[3];
             decode<D>(L, t, bb);
             correct_pt<D>(A->P[k], L, A->P[k + 1], Lc, bc, bb);
         }
+        sync();
+        for (int it = 0; it < A->s; ++it)
+            for (int j = 0; j < A->nm; ++j) {
+                const Lvl Lk = A->L[k];
+                for (long t = gtid; t < Lk.nblk; t += gstr) {
+                    int bb[3];
+                    decode<D>(Lk, t, bb);
+                    sweep_dispatch<D>(A->masks[j], A->P[k], A->F[k], Lk, bc, bb);
+                }
+                sync();
+            }
+    }
+}
+
+// Levels k0..k1-1 run on the whole cluster; levels k1..nl-1 (at most
+// ~one block per thread) on CTA 0 alone with CTA barriers, which are an
+// order of magnitude cheaper than cluster barriers.
+template <int D>
+__global__ void __launch_bounds__(512) k_coarse_cycle(const CoarseArgs* __restrict__ A) {
+    const unsigned rank = cluster_rank();
+    const long gtid = (long)rank * blockDim.x + threadIdx.x;
+    const long gstr = (long)cluster_size() * blockDim.x;
+    const int k0 = A->k0, k1 = A->k1, nl = A->nl;
+    run_levels<D, true>(A, k0, k1, false, gtid, gstr);
+    if (rank == 0) {
+        run_levels<D, false>(A, k1, nl - 1, true, threadIdx.x, blockDim.x);
+        run_ascent<D, false>(A, k1, nl - 1, threadIdx.x, blockDim.x);
+    }
+    if (k1 > k0) {
         cluster_sync_all();
-        smooth(k);
+        run_ascent<D, true>(A, k0, k1, gtid, gstr);
     }
 }

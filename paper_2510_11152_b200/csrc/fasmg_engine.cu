@@ -1293,6 +1293,9 @@ static int coarse_setup(Engine& E) {
     }
     h.bc = E.bc;
     h.k0 = k0;
+    int k1 = E.nl - 1;  // first level small enough for one CTA (<= ~2 blocks per thread)
+    while (k1 > k0 && E.L[k1 - 1].nblk <= 1024) --k1;
+    h.k1 = k1;
     h.nl = E.nl;
     h.s = E.s;
     h.nm = (int)E.masks.size();
