@@ -99,6 +99,7 @@ __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
 #include "fasmg_stencil.cuh"
 #include "fasmg_wave.cuh"
 #include "fasmg_coarse.cuh"
+#include "fasmg_fused.cuh"
 
 // ------------------------------------------------- edge-centered transfers
 // Reader of raw stored values at core (grid) index x in the blocked layout.
@@ -744,6 +745,12 @@ struct Engine {
     int coarse_cs = 8;                  // FASMG_COARSE_CS: CTAs per cluster
     long coarse_max = 4096;             // FASMG_COARSE_MAX: max blocks of a coarse level
     CoarseArgs* dcoarse = nullptr;      // device copy of the level table
+    // ---- last half-sweep fused with the residual (fasmg_fused.cuh) ----
+    int fuse = 0;                       // FASMG_FUSE bits: 1 tau pass, 2 outer norm (measured slower: off)
+    bool fuse_ok[32] = {};
+    CUtensorMap mapR[32], mapG[32];     // P boxes 36x12, F boxes 36x10
+    int npart_fused = 0;                // partial sums written by the fused norm
+    double* dbg = nullptr;              // FASMG_FUSE_DEBUG: per-point fused residual (level 0)
 };
 
 struct Tile {
@@ -1047,21 +1054,65 @@ static bool wave_seq(const Engine& E, int k, std::vector<unsigned>& seq) {
     return true;
 }
 
+// skip_last: leave the stage's final half-sweep to a fused kernel
 template <int D>
-static void launch_smooth(Engine& E, int k, long& cnt) {
+static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false) {
     std::vector<unsigned> seq;
     if (D == 3 && wave_seq(E, k, seq)) {
-        const int n = (int)seq.size();
+        const int n = (int)seq.size() - (skip_last ? 1 : 0);
         for (int i = 0; i < n; i += E.wave_T) launch_wave(E, k, seq, i, std::min(E.wave_T, n - i), cnt);
         return;
     }
     const Tile t = tile_of(E.L[k]);
+    const int total = E.s * (int)E.masks.size();
+    int done = 0;
     for (int it = 0; it < E.s; ++it)
         for (unsigned m : E.masks) {
+            if (skip_last && ++done == total) return;
             EA_DISPATCH(D, E.ea, (sweep_mask<D, EA>(E, k, m, t)));
             ++cnt;
             halo_exchange<D>(E, k, m, cnt);
         }
+}
+
+// can level k's last smoothing half-sweep run fused with the residual?
+static bool fused_level(const Engine& E, int k, int mode_bit = 1) {
+    if (!(E.fuse & mode_bit) || !E.fuse_ok[k] || E.masks.empty()) return false;
+    const unsigned m = E.masks.back();
+    return m == 0x96u || m == 0x69u;
+}
+
+static dim3 fused_grid(const Lvl& L, int* chunk_out, int march_chunk) {
+    using namespace fsw;
+    const long tiles = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
+    int chunk = march_chunk;
+    if (chunk <= 0) {
+        chunk = 4;
+        for (int c = 16; c >= 8; c >>= 1)
+            if (tiles * ((L.B[0] + c - 1) / c) >= 592) { chunk = c; break; }
+    }
+    *chunk_out = chunk;
+    return dim3((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
+}
+
+template <int MODE>
+static void launch_fused(Engine& E, int k, long& cnt) {
+    const Lvl& L = E.L[k];
+    const Lvl& Lc = MODE == fsw::MODE_TAU ? E.L[k + 1] : L;
+    double* Pc = MODE == fsw::MODE_TAU ? E.P[k + 1] : nullptr;
+    double* Fc = MODE == fsw::MODE_TAU ? E.F[k + 1] : E.dbg;
+    int chunk = 0;
+    const dim3 grd = fused_grid(L, &chunk, E.march_chunk);
+    const dim3 blk(fsw::TX, fsw::TY, 1);
+    const Lvl& Ld = L;
+    if (E.masks.back() == 0x96u)
+        k_sweep_resid<MODE, 0x96u><<<grd, blk, fsw::SMEM, E.stream>>>(
+            E.mapR[k], E.mapG[k], E.mapF[k], E.P[k], Ld, E.bc, chunk, E.part, Pc, Fc, Lc);
+    else
+        k_sweep_resid<MODE, 0x69u><<<grd, blk, fsw::SMEM, E.stream>>>(
+            E.mapR[k], E.mapG[k], E.mapF[k], E.P[k], Ld, E.bc, chunk, E.part, Pc, Fc, Lc);
+    ++cnt;
+    launch_pad_fill<3>(E, k, cnt);  // the deferred ghost pads of the new B values
 }
 
 template <int D>
@@ -1081,8 +1132,10 @@ static void launch_coarse(Engine& E, long& cnt) {
     ++cnt;
 }
 
+// fuse_norm: the finest level's last half-sweep also produces the outer
+// residual's partial sums (launch_norm then only reduces them)
 template <int D>
-static void launch_vcycle(Engine& E, long& cnt) {
+static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
     const unsigned ALL = (1u << (1 << D)) - 1;
     // levels >= kc run inside one cluster launch
     const int kc = E.coarse_k0 >= 0 ? E.coarse_k0 : E.nl;
@@ -1095,11 +1148,18 @@ static void launch_vcycle(Engine& E, long& cnt) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L), tc = tile_of(Lc);
-        launch_smooth<D>(E, k, cnt);
+        if (D == 3 && fused_level(E, k)) {
+            launch_smooth<D>(E, k, cnt, true);
+            launch_fused<fsw::MODE_TAU>(E, k, cnt);
+        } else {
+            launch_smooth<D>(E, k, cnt);
+        }
         if (E.ea < 0) {
-            k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.P[k + 1],
-                                                             E.F[k + 1], Lc, E.bc);
-            ++cnt;
+            if (!(D == 3 && fused_level(E, k))) {
+                k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.P[k + 1],
+                                                                 E.F[k + 1], Lc, E.bc);
+                ++cnt;
+            }
         } else {
             EA_DISPATCH(D, E.ea, (k_residual_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
                                      E.P[k], E.F[k], E.R[k], L)));
@@ -1159,18 +1219,41 @@ static void launch_vcycle(Engine& E, long& cnt) {
             launch_pad_fill<D>(E, k, cnt);
         }
         halo_exchange<D>(E, k, ALL, cnt);
-        launch_smooth<D>(E, k, cnt);
+        if (k == 0 && fuse_norm) {
+            launch_smooth<D>(E, k, cnt, true);
+            launch_fused<fsw::MODE_NORM>(E, k, cnt);
+        } else {
+            launch_smooth<D>(E, k, cnt);
+        }
     }
 }
 
 template <int D>
-static void launch_norm(Engine& E, long& cnt) {
+static bool norm_fusable(const Engine& E) {
+    return D == 3 && E.nl > 1 && E.coarse_k0 != 0 && fused_level(E, 0, 2);
+}
+
+template <int D>
+static void launch_norm(Engine& E, long& cnt, bool fused = false) {
     const Lvl& L = E.L[0];
     const Tile t = tile_of(L);
-    EA_DISPATCH(D, E.ea, (k_res_sumsq_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
-                             E.P[0], E.F[0], L, E.part)));
-    k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, E.npart, E.dsum);
-    cnt += 2;
+    int npart_norm = E.npart;
+    if (!fused) {
+        if (E.ea < 0) {
+            // (walking axis 0 in chunks per thread measured slower: 1 block)
+            const int ch = 1;
+            Tile tt = t;
+            if (D == 3) tt.grid.z = (L.B[0] + ch * tt.block.z - 1) / (ch * tt.block.z);
+            k_res_sumsq_cell<D><<<tt.grid, tt.block, 0, E.stream>>>(E.P[0], E.F[0], L, E.part,
+                                                                     ch);
+            npart_norm = (int)tile_ctas(tt);
+        } else
+            EA_DISPATCH(D, E.ea, (k_res_sumsq_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
+                                     E.P[0], E.F[0], L, E.part)));
+        ++cnt;
+    }
+    k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, fused ? E.npart_fused : npart_norm, E.dsum);
+    ++cnt;
     if (E.nranks > 1) {  // fixed rank-order sum of the partials on every rank
         const int P = E.nranks, r = E.rank;
         for (int q = 0; q < P; ++q) {
@@ -1196,8 +1279,9 @@ static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* e
     cudaError_t e = cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return fasmg_check(e);
     if (E.dim == 3) {
-        launch_vcycle<3>(E, cnt);
-        if (with_norm) launch_norm<3>(E, cnt);
+        const bool fz = with_norm && norm_fusable<3>(E);
+        launch_vcycle<3>(E, cnt, fz);
+        if (with_norm) launch_norm<3>(E, cnt, fz);
     } else {
         launch_vcycle<2>(E, cnt);
         if (with_norm) launch_norm<2>(E, cnt);
@@ -1309,6 +1393,50 @@ static int coarse_setup(Engine& E) {
     }
     if (!st) E.coarse_k0 = k0;
     return st;
+}
+
+template <int MODE>
+static int fused_attr() {
+    const int sm = (int)fsw::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_resid<MODE, 0x96u>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep_resid<MODE, 0x69u>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return fasmg_check(e);
+}
+
+// levels whose last half-sweep fuses with the residual: 3D cell-centred,
+// unsharded TMA levels, no periodic face (FASMG_FUSE=0 disables)
+static int fused_setup(Engine& E) {
+    if (const char* v = getenv("FASMG_FUSE")) E.fuse = atoi(v);
+    if (!E.fuse || E.dim != 3 || E.ea >= 0) return 0;
+    for (int a = 0; a < 3; ++a)
+        if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return 0;
+    bool any = false;
+    for (int k = 0; k < E.nl - 1; ++k) {
+        if (!E.tma_ok[k] || E.sharded(k)) continue;
+        const Lvl& L = E.L[k];
+        E.fuse_ok[k] = encode_map(&E.mapR[k], E.P[k], L, fsw::AX, fsw::AY) &&
+                       encode_map(&E.mapG[k], E.F[k], L, fsw::FX, fsw::FY);
+        any = any || E.fuse_ok[k];
+    }
+    if (!any) return 0;
+    int st = fused_attr<fsw::MODE_NORM>();
+    if (!st) st = fused_attr<fsw::MODE_TAU>();
+    if (st) return st;
+    if (getenv("FASMG_FUSE_DEBUG")) {
+        size_t bytes = sizeof(double) * (size_t)E.L[0].cls * 8;
+        if (int st = fasmg_check(cudaMalloc(&E.dbg, bytes))) return st;
+        cudaMemsetAsync(E.dbg, 0, bytes, E.stream);
+    }
+    if (E.fuse_ok[0]) {
+        int chunk = 0;
+        const dim3 g = fused_grid(E.L[0], &chunk, E.march_chunk);
+        E.npart_fused = (int)(g.x * g.y * g.z);
+        if (E.npart_fused > E.npart) return fasmg_set_error(FASMG_EINVAL, "fused norm partials exceed buffer");
+    }
+    return 0;
 }
 
 static int wave_setup(Engine& E) {
@@ -1485,8 +1613,9 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         }
         for (int t = 0; t < dim; ++t) nn[t] /= 2;
     }
-    if (int st = wave_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (TMA maps, coarse cluster, wavefront) failed"); return nullptr; }
     E->npart = (int)tile_ctas(tile_of(E->L[0]));
+    if (int st = wave_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (TMA maps, coarse cluster, wavefront) failed"); return nullptr; }
+    if (int st = fused_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (fused residual) failed"); return nullptr; }
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
         fasmg_check(cudaMallocHost(&E->hsum, sizeof(double))) ||
@@ -1670,8 +1799,9 @@ int fasmg_engine_run(void* h, int count, int with_norm, double* sumsq, int use_g
         } else {
             long cnt = 0;
             if (E->dim == 3) {
-                launch_vcycle<3>(*E, cnt);
-                if (with_norm) launch_norm<3>(*E, cnt);
+                const bool fz = with_norm && norm_fusable<3>(*E);
+                launch_vcycle<3>(*E, cnt, fz);
+                if (with_norm) launch_norm<3>(*E, cnt, fz);
             } else {
                 launch_vcycle<2>(*E, cnt);
                 if (with_norm) launch_norm<2>(*E, cnt);
@@ -1725,7 +1855,8 @@ int fasmg_engine_level_geom(void* h, int k, long* out) {
 int fasmg_engine_level_copy(void* h, int k, int which, double* dst) {
     Engine* E = (Engine*)h;
     if (k < 0 || k >= E->nl) return fasmg_set_error(FASMG_EINVAL, "level out of range");
-    const double* src = which == 0 ? E->P[k] : E->F[k];
+    const double* src = which == 0 ? E->P[k] : (which == 1 ? E->F[k] : E->dbg);
+    if (!src) return fasmg_set_error(FASMG_EINVAL, "no such array");
     int st = fasmg_check(cudaStreamSynchronize(E->stream));
     if (st) return st;
     return fasmg_check(cudaMemcpy(dst, src, sizeof(double) * E->L[k].cls * (1u << E->dim),

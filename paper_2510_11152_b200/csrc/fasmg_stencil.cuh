@@ -717,6 +717,81 @@ __global__ void __launch_bounds__(256) k_residual_fast(const double* __restrict_
     }
 }
 
+// Outer residual sum of squares of a cell-centred level, structured like
+// k_tau_fast: every load of the block (2^d centers, 2^d f, d*2^(d-1)
+// across-face neighbours) is issued before any arithmetic, so a warp keeps
+// ~3x more DRAM requests in flight than the per-class op_fast loop.  Same
+// per-point arithmetic (op_fast order), same per-CTA fixed-order partials.
+template <int D>
+__global__ void __launch_bounds__(256) k_res_sumsq_cell(const double* __restrict__ P,
+                                                        const double* __restrict__ F, Lvl L,
+                                                        double* __restrict__ part, int chunk) {
+    int bb[3];
+    double acc = 0.0;
+    const bool act = tile_coords<D>(L, bb);
+    // each thread walks `chunk` consecutive blocks along axis 0 (fewer CTAs,
+    // one CTA reduction per chunk)
+    const int b0s = (bb[0] - 1) * chunk + 1;
+    for (int i = 0; act && i < chunk && b0s + i <= L.B[0]; ++i) {
+        bb[0] = b0s + i;
+        constexpr int NC = 1 << D;
+        const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+        double pc[NC], fv[NC], out[NC][D];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const long o = o0 + (long)c * L.cls;
+            pc[c] = __ldg(P + o);
+            fv[c] = __ldg(F + o);
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int bit = 1 << (D - 1 - a);
+                const long dcls = (long)((c ^ bit) - c) * L.cls;
+                const long sa = bstride<D>(L, a);
+                out[c][a] = (c & bit) ? __ldg(P + o + dcls - sa) : __ldg(P + o + dcls + sa);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            double ns = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int bit = 1 << (D - 1 - a);
+                const double inside = pc[c ^ bit];
+                const double e = (c & bit) ? inside : out[c][a];
+                const double w = (c & bit) ? out[c][a] : inside;
+                ns = a == 0 ? ad(e, w) : ad(ad(ns, e), w);
+            }
+            const double lap = ml(sb(ns, ml(D == 3 ? 6.0 : 4.0, pc[c])), L.inv_h2);
+            const double r = sb(fv[c], sb(ml(L.a, pc[c]), ml(L.b, lap)));
+            acc = ad(acc, ml(r, r));
+        }
+    }
+    // fixed-order CTA reduction: xor-shuffle tree per warp, then the warp
+    // sums in order (CTAs of whole warps); else a shared-memory tree
+    __shared__ double red[256];
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nt = blockDim.x * blockDim.y * blockDim.z;
+    const long pid = blockIdx.x + gridDim.x * (blockIdx.y + (long)gridDim.y * blockIdx.z);
+    if (nt % 32 == 0) {
+        for (int m = 16; m > 0; m >>= 1) acc = ad(acc, __shfl_xor_sync(0xffffffffu, acc, m));
+        if ((tid & 31) == 0) red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double t = red[0];
+            for (int w = 1; w < nt / 32; ++w) t = ad(t, red[w]);
+            part[pid] = t;
+        }
+        return;
+    }
+    red[tid] = acc;
+    __syncthreads();
+    for (int s = nt >> 1; s > 0; s >>= 1) {
+        if (tid < s) red[tid] = ad(red[tid], red[tid + s]);
+        __syncthreads();
+    }
+    if (tid == 0) part[pid] = red[0];
+}
+
 // outer residual sum of squares: per-CTA fixed-order partials
 template <int D, int EA>
 __global__ void __launch_bounds__(256) k_res_sumsq_fast(const double* __restrict__ P,

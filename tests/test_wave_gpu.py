@@ -29,6 +29,9 @@ LOC = {"cell": "CELL", "edge_ew": "EDGE_EW", "edge_ns": "EDGE_NS", "edge_tb": "E
 
 FACES = {
     "dirichlet": None,
+    "mixed_dn": {"xlo": ("dirichlet", 0.25), "xhi": ("neumann", 0.0),
+                 "ylo": ("neumann", 0.0), "yhi": ("dirichlet", 0.5),
+                 "zlo": ("dirichlet", -1.0), "zhi": ("neumann", 0.0)},
     "lid": None,
     # y periodic (in-plane wrap), x / z mixed Dirichlet values and Neumann
     "mixed_yz": {"xlo": ("dirichlet", 0.25), "xhi": ("neumann", 0.0),
@@ -134,3 +137,32 @@ def test_tma_sweep_vs_oracle(P, monkeypatch, shape, loc, spec):
                        faces, p0, f0, ml, 2)
     np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
     assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+
+
+@pytest.mark.parametrize("shape,spec,env", [
+    ((64, 64, 64), "dirichlet", {}),
+    ((48, 112, 80), "mixed_dn", {}),                       # partial tile along b2
+    ((96, 64, 128), "mixed_dn", {"FASMG_MARCH_CHUNK": 5}),  # ragged chunks
+    ((64, 64, 64), "lid", {"FASMG_MARCH_CHUNK": 1}),
+])
+def test_fused_sweep_residual_vs_oracle(P, monkeypatch, shape, spec, env):
+    """k_sweep_resid (last half-sweep fused with the tau pass and with the
+    outer residual norm) forced onto small levels: fields bitwise equal to
+    the oracle, residual history within 1e-10."""
+    import oracle as O
+    faces = faces_of(spec)
+    ml = 3
+    p0 = C.rand_field(51, shape, "cell", 1)
+    f0 = C.rand_field(52, shape, "cell", 1)
+    op = O.OField(shape, "cell", 1, p0.copy())
+    of = O.OField(shape, "cell", 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 3, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    e = {"FASMG_TMA_MIN": 0, **env}
+    got, rep = run_gpu(P, monkeypatch, e, shape, "cell", faces, p0, f0, ml, 3)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+    off, rep2 = run_gpu(P, monkeypatch, {**e, "FASMG_FUSE": 0}, shape, "cell", faces, p0, f0, ml, 3)
+    assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
