@@ -669,6 +669,7 @@ __global__ void k_wait(const long long* __restrict__ my_slot, long long* __restr
         // a peer that never arrives is a protocol bug: fail loudly (~30 s)
         // instead of hanging the device
         if (clock64() - t0 > 60000000000LL) asm volatile("trap;");
+        if (v < e) __nanosleep(100);  // back off: keep the memory system free for the peers
     } while (v < e);
     __threadfence_system();
 }
@@ -1364,7 +1365,11 @@ static int tma_setup(Engine& E) {
 static int coarse_setup(Engine& E) {
     if (const char* v = getenv("FASMG_COARSE_MAX")) E.coarse_max = atol(v);
     if (const char* v = getenv("FASMG_COARSE_CS")) E.coarse_cs = std::max(1, std::min(16, atoi(v)));
-    if (E.ea >= 0 || E.coarse_max <= 0 || E.masks.size() > 16) return 0;
+    // Not with slab ranks: the cluster launch needs 8 whole SMs of one GPC
+    // at once (512 threads x 128 registers each); with virtual ranks sharing
+    // a device it can starve behind peers' spin-waits (observed: 8 virtual
+    // ranks at 512^3).  Sharded engines keep per-level launches.
+    if (E.ea >= 0 || E.coarse_max <= 0 || E.masks.size() > 16 || E.nranks > 1) return 0;
     int k0 = E.nl;
     while (k0 > 0 && !E.sharded(k0 - 1) && E.L[k0 - 1].nblk <= E.coarse_max) --k0;
     if (k0 >= E.nl) return 0;

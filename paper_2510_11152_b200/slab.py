@@ -164,6 +164,7 @@ class VirtualSlabSolver:
         self.hierarchy, self.location, self.bc = hierarchy, location, bc
         self.plan, self.coeffs, self.parts, self.min_planes = plan, coeffs, parts, min_planes
         self._engines = {}
+        self._pool = None
 
     def engines(self, s: int, device: torch.device):
         key = (int(s), device.index)
@@ -177,6 +178,19 @@ class VirtualSlabSolver:
                 e.connect(exports)
             self._engines[key] = es
         return es
+
+    def launch_all(self, es, count: int, with_norm: bool):
+        """Enqueue every virtual rank's graph from its own host thread: a
+        graph launch may block the host once its stream's queue is full,
+        and a rank's graph stalls on device until its peers' graphs run --
+        launching the ranks one after another from one thread can deadlock
+        (observed with 8 ranks at 512^3).  ctypes releases the GIL."""
+        if self._pool is None:
+            import concurrent.futures as cf
+            self._pool = cf.ThreadPoolExecutor(max_workers=self.parts)
+        futs = [self._pool.submit(e.launch, count, with_norm) for e in es]
+        for fu in futs:
+            fu.result()
 
     def _singular(self):
         return self.coeffs.a == 0.0 and all(r.kind != "dirichlet" for _, r in self.bc.faces)
@@ -200,8 +214,7 @@ class VirtualSlabSolver:
     def vcycle(self, p: Field, f: Field, s: int) -> Field:
         es = self.engines(s, p.device)
         self._load(es, p, f)
-        for e in es:
-            e.launch(1, False)
+        self.launch_all(es, 1, False)
         for e in es:
             e.synchronize()
         self._store(es, p)
@@ -218,8 +231,7 @@ class VirtualSlabSolver:
         scale = g.h ** (g.dim / 2.0)
         history = []
         for _ in range(params.k_max):
-            for e in es:
-                e.launch(1, True)
+            self.launch_all(es, 1, True)
             sums = [e.result() for e in es]
             if any(x != sums[0] for x in sums):
                 raise NativeError(f"ranks disagree on the residual: {sums}")

@@ -45,3 +45,30 @@ def test_virtual_slabs_match_single(P, n, dim, parts, bc, a):
     np.testing.assert_allclose(rep2.residual_history, rep1.residual_history, rtol=1e-12)
     assert torch.equal(p1.data, p2.data)
     assert torch.equal(f1.data, f2.data)
+
+
+@pytest.mark.parametrize("n,parts", [(128, 2), (128, 4), (128, 8), (256, 8)])
+def test_virtual_slabs_tma_levels(P, monkeypatch, n, parts):
+    """Sharded levels on the TMA march (FASMG_TMA_MIN=0 forces it onto small
+    slabs): bitwise equal to the single-engine solve."""
+    from paper_2510_11152_b200.slab import VirtualSlabSolver
+    import cases as C
+    monkeypatch.setenv("FASMG_TMA_MIN", "0")
+    shape = (n,) * 3
+    ml = int(np.log2(n)) - 1
+    p0 = C.rand_field(61, shape, "cell", 1)
+    f0 = C.rand_field(62, shape, "cell", 1)
+    g = P.unit_grid(shape)
+    bc = P.BoundaryCondition.dirichlet(3)
+    coeffs = P.OperatorCoeffs(1.0, 0.5)
+    plan = P.make_plan("x", 3)
+    params = P.FasParams(1e-30, 2, 2, ml)
+    p1 = P.Field(g, P.Location.CELL, 1, p0.copy())
+    f1 = P.Field(g, P.Location.CELL, 1, f0.copy())
+    rep1 = P.FasSolver(P.make_hierarchy(g, ml), P.Location.CELL, bc, plan, coeffs).solve(p1, f1, params)
+    p2 = P.Field(g, P.Location.CELL, 1, p0.copy())
+    f2 = P.Field(g, P.Location.CELL, 1, f0.copy())
+    vs = VirtualSlabSolver(P.make_hierarchy(g, ml), P.Location.CELL, bc, plan, coeffs, parts)
+    rep2 = vs.solve(p2, f2, params)
+    np.testing.assert_allclose(rep2.residual_history, rep1.residual_history, rtol=1e-12)
+    assert torch.equal(p1.data, p2.data)
