@@ -833,13 +833,12 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
     }
     if (D == 3 && E.sweep_variant == 4 && E.tma_ok[k] && __builtin_popcount(M) > 1) {
         using namespace tsw;
-        const long tiles = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
-        int chunk = E.march_chunk;
-        if (chunk <= 0) {
-            chunk = 4;
-            for (int c = 16; c >= 8; c >>= 1)
-                if (tiles * ((L.B[0] + c - 1) / c) >= 1184) { chunk = c; break; }
-        }
+        // 4-plane chunks: 16384 CTAs at 512^3; the 2 window planes a chunk
+        // re-loads are L2 hits of the neighbouring chunk's CTAs (ncu: 1.63 GB
+        // per finest launch vs 1.69 GB at 16 planes), and the many short
+        // CTAs keep every SM's TMA queue full to the end of the launch:
+        // 276 -> 248 us (B200, profiles/r01g_ncu_summary.txt)
+        const int chunk = E.march_chunk > 0 ? E.march_chunk : 4;
         dim3 blk(TX, TY, 1);
         dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
         k_sweep_tma<EA, M><<<grd, blk, SMEM, E.stream>>>(E.mapT[k], E.mapF[k], E.P[k], L, E.bc,

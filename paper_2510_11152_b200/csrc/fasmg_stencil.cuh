@@ -766,30 +766,17 @@ __global__ void __launch_bounds__(256) k_res_sumsq_cell(const double* __restrict
             acc = ad(acc, ml(r, r));
         }
     }
-    // fixed-order CTA reduction: xor-shuffle tree per warp, then the warp
-    // sums in order (CTAs of whole warps); else a shared-memory tree
+    // fixed-order tree over the CTA (block sizes are powers of two <= 256)
     __shared__ double red[256];
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const int nt = blockDim.x * blockDim.y * blockDim.z;
-    const long pid = blockIdx.x + gridDim.x * (blockIdx.y + (long)gridDim.y * blockIdx.z);
-    if (nt % 32 == 0) {
-        for (int m = 16; m > 0; m >>= 1) acc = ad(acc, __shfl_xor_sync(0xffffffffu, acc, m));
-        if ((tid & 31) == 0) red[tid >> 5] = acc;
-        __syncthreads();
-        if (tid == 0) {
-            double t = red[0];
-            for (int w = 1; w < nt / 32; ++w) t = ad(t, red[w]);
-            part[pid] = t;
-        }
-        return;
-    }
     red[tid] = acc;
     __syncthreads();
     for (int s = nt >> 1; s > 0; s >>= 1) {
         if (tid < s) red[tid] = ad(red[tid], red[tid + s]);
         __syncthreads();
     }
-    if (tid == 0) part[pid] = red[0];
+    if (tid == 0) part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = red[0];
 }
 
 // outer residual sum of squares: per-CTA fixed-order partials
