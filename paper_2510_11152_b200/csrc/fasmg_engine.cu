@@ -740,7 +740,8 @@ struct Engine {
     unsigned* wave_buf = nullptr;       // ticket + [T][B0+2] completion counters
     bool wave_ok[32] = {};
     bool tma_ok[32] = {};               // level k half-sweeps use k_sweep_tma
-    CUtensorMap mapH[32], mapI[32], mapF[32], mapT[32];
+    CUtensorMap mapH[32], mapI[32], mapF[32], mapT[32], mapP8[32];
+    int resid_tma = 1;                  // FASMG_RESID_TMA: tau / norm on the TMA march
     // ---- coarse levels in one cluster launch (fasmg_coarse.cuh) ----
     int coarse_k0 = -1;                 // first level run by k_coarse_cycle (-1: none)
     int coarse_cs = 8;                  // FASMG_COARSE_CS: CTAs per cluster
@@ -757,6 +758,16 @@ struct Engine {
 struct Tile {
     dim3 grid, block;
 };
+
+// tau / outer norm of level k on the TMA march (cell-centred, unsharded)
+static bool resid_tma_level(const Engine& E, int k) {
+    return E.resid_tma && E.dim == 3 && E.ea < 0 && E.tma_ok[k] && !E.sharded(k);
+}
+
+static dim3 resid_grid(const Lvl& L, int chunk) {
+    using namespace rsw;
+    return dim3((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
+}
 
 static unsigned p2ceil(unsigned v) {
     unsigned r = 1;
@@ -1156,8 +1167,16 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
         }
         if (E.ea < 0) {
             if (!(D == 3 && fused_level(E, k))) {
-                k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.P[k + 1],
-                                                                 E.F[k + 1], Lc, E.bc);
+                if (D == 3 && resid_tma_level(E, k)) {
+                    const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+                    k_resid_tma<1><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
+                                     E.stream>>>(E.mapT[k], E.mapP8[k], E.F[k], L, E.bc, ch,
+                                                 nullptr, E.P[k + 1], E.F[k + 1], Lc);
+                } else {
+                    k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L,
+                                                                     E.P[k + 1], E.F[k + 1], Lc,
+                                                                     E.bc);
+                }
                 ++cnt;
             }
         } else {
@@ -1239,7 +1258,13 @@ static void launch_norm(Engine& E, long& cnt, bool fused = false) {
     const Tile t = tile_of(L);
     int npart_norm = E.npart;
     if (!fused) {
-        if (E.ea < 0) {
+        if (D == 3 && resid_tma_level(E, 0)) {
+            const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+            const dim3 g = resid_grid(L, ch);
+            k_resid_tma<0><<<g, dim3(rsw::TX, rsw::TY, 1), rsw::SMEM, E.stream>>>(
+                E.mapT[0], E.mapP8[0], E.F[0], L, E.bc, ch, E.part, nullptr, nullptr, L);
+            npart_norm = (int)(g.x * g.y * g.z);
+        } else if (E.ea < 0) {
             // (walking axis 0 in chunks per thread measured slower: 1 block)
             const int ch = 1;
             Tile tt = t;
@@ -1350,14 +1375,23 @@ static int tma_setup(Engine& E) {
         const Lvl& L = E.L[k];
         if (L.B[2] < 32 || L.B[1] < 8 || L.nblk < min_blocks) continue;
         E.tma_ok[k] = encode_map(&E.mapT[k], E.P[k], L, tsw::HX, tsw::HY) &&
-                      encode_map(&E.mapF[k], E.F[k], L, tsw::TX, tsw::TY);
+                      encode_map(&E.mapF[k], E.F[k], L, tsw::TX, tsw::TY) &&
+                      encode_map(&E.mapP8[k], E.P[k], L, tsw::TX, tsw::TY);
         any = any || E.tma_ok[k];
     }
     if (!any) return 0;
+    if (const char* v = getenv("FASMG_RESID_TMA")) E.resid_tma = atoi(v);
     int st = 0;
     EA_DISPATCH(3, E.ea, (st = tma_attr<EA>()));
+    if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<0>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)rsw::SMEM));
+    if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)rsw::SMEM));
     return st;
 }
+
 
 // Levels from coarse_k0 down run in k_coarse_cycle: cell-centered, not
 // sharded, at most coarse_max blocks.

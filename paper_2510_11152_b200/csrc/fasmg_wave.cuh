@@ -446,3 +446,121 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
         __syncthreads();  // the next prefetch overwrites this step's oldest slots
     }
 }
+
+// ---------------------------------------------------------------------------
+// Residual of a cell-centred level on the same TMA march (k_sweep_tma's
+// tile/chunk geometry): per plane step one thread issues, for each of the
+// 8 classes, the plane-b0 tile with its in-plane halo (36 x 10), the one
+// axis-0 neighbour plane the opposite-q0 classes need (32 x 8, b0+1 for
+// q0=1 classes, b0-1 for q0=0), double-buffered on two mbarriers; f is
+// read straight from global (issued before the barrier wait).  MODE 0 accumulates sum(r^2) (outer norm, PKG/fas.py:149-151;
+// per-CTA fixed-order partials); MODE 1 restricts r and p into the coarse
+// level (tau pass, PKG/fas.py:99-107) with tau_pt's exact arithmetic.
+namespace rsw {
+constexpr int TX = 32, TY = 8, HX = TX + 4, HB = 384, IB = TX * TY;
+constexpr size_t SLOT = (size_t)8 * HB + 8 * IB;  // halo boxes + axis-0 neighbour boxes
+constexpr size_t SMEM = 2 * SLOT * 8 + 2 * 8;
+constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u + 8u * IB * 8u;
+}  // namespace rsw
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUtensorMap mapH,
+                                                   const __grid_constant__ CUtensorMap mapI,
+                                                   const double* __restrict__ F, Lvl L,
+                                                   BcSpec bc, int chunk,
+                                                   double* __restrict__ part,
+                                                   double* __restrict__ Pc,
+                                                   double* __restrict__ Fc, Lvl Lc) {
+    using namespace rsw;
+    extern __shared__ __align__(128) double sm[];
+    unsigned long long* bar = (unsigned long long*)(sm + 2 * SLOT);
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int x0 = blockIdx.x * TX + 1, y0 = blockIdx.y * TY + 1;
+    const int b0s = 1 + blockIdx.z * chunk;
+    const int b0e = min(L.B[0], b0s + chunk - 1);
+    auto issue = [&](int b0, int s) {
+        double* S = sm + s * SLOT;
+        mbar_expect_tx(&bar[s], TXB);
+        for (int k = 0; k < 8; ++k) {
+            tma_load4(S + k * HB, &mapH, &bar[s], OFF + x0 - 2, y0 - 1, b0, k);
+            tma_load4(S + 8 * HB + k * IB, &mapI, &bar[s], OFF + x0, y0, (k & 4) ? b0 + 1 : b0 - 1,
+                      k);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue(b0s, 0);
+    }
+    __syncthreads();
+    const int b1 = y0 + ty, b2 = x0 + tx;
+    const bool active = b1 <= L.B[1] && b2 <= L.B[2];
+    const int ci = (ty + 1) * HX + tx + 2;  // tile centre in a halo box
+    double acc = 0.0;
+    for (int b0 = b0s; b0 <= b0e; ++b0) {
+        const int s = (b0 - b0s) & 1;
+        if (tid == 0 && b0 < b0e) issue(b0 + 1, s ^ 1);
+        double fv[8];
+        if (active) {
+            const long o = at<3>(L, 0, b0, b1, b2);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) fv[c] = __ldg(F + o + (long)c * L.cls);
+        }
+        mbar_wait(&bar[s], ((b0 - b0s) >> 1) & 1);
+        const double* S = sm + s * SLOT;
+        if (active) {
+            double pc[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) pc[c] = S[c * HB + ci];
+            double rp = 0.0, rr = 0.0;
+#pragma unroll
+            for (int c = 7; c >= 0; --c) {
+                double ns = 0.0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const int bit = 1 << (2 - a);
+                    const bool qa = (c & bit) != 0;
+                    const int k = c ^ bit;
+                    const double inside = pc[k];
+                    // across the block face: W of q=1, E of q=0
+                    double out;
+                    if (a == 0) out = S[8 * HB + k * IB + tid];
+                    else if (a == 1) out = S[k * HB + ci + (qa ? -HX : HX)];
+                    else out = S[k * HB + ci + (qa ? -1 : 1)];
+                    const double e = qa ? inside : out;
+                    const double w = qa ? out : inside;
+                    ns = a == 0 ? ad(e, w) : ad(ad(ns, e), w);
+                }
+                const double lap = ml(sb(ns, ml(6.0, pc[c])), L.inv_h2);
+                const double r = sb(fv[c], sb(ml(L.a, pc[c]), ml(L.b, lap)));
+                if (MODE == 0) {
+                    acc = ad(acc, ml(r, r));
+                } else {
+                    if (c == 7) { rp = pc[c]; rr = r; }
+                    else { rp = ad(rp, pc[c]); rr = ad(rr, r); }
+                }
+            }
+            if (MODE == 1) {
+                int bb[3] = {b0, b1, b2}, cc = 0, cb[3] = {0, 0, 0};
+                coarse_of<3>(L, Lc, bb, cc, cb);
+                const long oc = at<3>(Lc, cc, cb[0], cb[1], cb[2]);
+                const double pcv = ml(rp, 0.125);
+                Pc[oc] = pcv;
+                Fc[oc] = ml(rr, 0.125);
+                if (on_boundary<3>(Lc, cb)) write_pads<3, -1>(Pc, Lc, bc, cc, cb, oc, pcv);
+            }
+        }
+        __syncthreads();  // slot s is refilled by the next step's prefetch
+    }
+    if (MODE == 0) {
+        double* red = sm;  // the ring is free now
+        red[tid] = acc;
+        __syncthreads();
+        for (int s2 = 128; s2 > 0; s2 >>= 1) {
+            if (tid < s2) red[tid] = ad(red[tid], red[tid + s2]);
+            __syncthreads();
+        }
+        if (tid == 0) part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = red[0];
+    }
+}
