@@ -842,6 +842,15 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         k_sweep_march<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
         return;
     }
+    if (D == 2 && E.sweep_variant == 4 && E.tma_ok[k] && __builtin_popcount(M) > 1) {
+        using namespace tsw2;
+        const int steps = E.march_chunk > 0 ? E.march_chunk : 4;
+        dim3 blk(TX, TY, 1);
+        dim3 grd((L.B[1] + TX - 1) / TX, (L.B[0] + steps * TY - 1) / (steps * TY), 1);
+        k_sweep_tma2d<EA, M><<<grd, blk, SMEM, E.stream>>>(E.mapT[k], E.mapF[k], E.P[k], L,
+                                                           E.bc, steps);
+        return;
+    }
     if (D == 3 && E.sweep_variant == 4 && E.tma_ok[k] && __builtin_popcount(M) > 1) {
         using namespace tsw;
         // 4-plane chunks: 16384 CTAs at 512^3; the 2 window planes a chunk
@@ -1344,6 +1353,26 @@ static bool encode_map(CUtensorMap* m, double* base, const Lvl& L, unsigned bx, 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2D levels: the class arrays as a 3D tensor (pitch, E0, class)
+static bool encode_map2d(CUtensorMap* m, double* base, const Lvl& L, unsigned bx, unsigned by) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)L.s0, (cuuint64_t)L.E[0], 4};
+    cuuint64_t strides[2] = {(cuuint64_t)L.s0 * 8, (cuuint64_t)L.cls * 8};
+    cuuint32_t box[3] = {bx, by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Decide which levels smooth by wavefront launches and prepare them.
 template <int EA>
 static int wave_attr(int* occ) {
@@ -1366,10 +1395,36 @@ static int tma_attr() {
 }
 
 // TMA maps of the levels whose half-sweeps run k_sweep_tma
+template <int EA>
+static int tma2d_attr() {
+    const int sm = (int)tsw2::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_tma2d<EA, 0x6u>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep_tma2d<EA, 0x9u>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return fasmg_check(e);
+}
+
 static int tma_setup(Engine& E) {
-    if (E.dim != 3 || E.sweep_variant != 4) return 0;
+    if (E.sweep_variant != 4) return 0;
     long min_blocks = 1L << 21;  // FASMG_TMA_MIN: smaller levels are launch-latency bound
     if (const char* v = getenv("FASMG_TMA_MIN")) min_blocks = atol(v);
+    if (E.dim == 2) {
+        bool any = false;
+        for (int k = 0; k < E.nl; ++k) {
+            const Lvl& L = E.L[k];
+            if (L.B[1] < 32 || L.B[0] < 8 || L.nblk < min_blocks) continue;
+            E.tma_ok[k] = encode_map2d(&E.mapT[k], E.P[k], L, tsw2::HX, tsw2::HY) &&
+                          encode_map2d(&E.mapF[k], E.F[k], L, tsw2::TX, tsw2::TY);
+            any = any || E.tma_ok[k];
+        }
+        if (!any) return 0;
+        int st = 0;
+        EA_DISPATCH(2, E.ea, (st = tma2d_attr<EA>()));
+        return st;
+    }
+    if (E.dim != 3) return 0;
     bool any = false;
     for (int k = 0; k < E.nl; ++k) {
         const Lvl& L = E.L[k];

@@ -564,3 +564,102 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
         if (tid == 0) part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = red[0];
     }
 }
+
+// ---------------------------------------------------------------------------
+// 2D half-sweep fed by TMA.  A CTA owns a 32 (b1) x 8 (b0) tile and walks
+// `steps` consecutive tiles down axis 0; per step ONE thread issues the two
+// opposite classes' tile + 1-block halo (36 x 10 box, 16-byte aligned start)
+// and f of the two updated classes (32 x 8), double-buffered on two
+// mbarriers so the next tile's loads overlap this tile's arithmetic.  Same
+// per-point arithmetic / pad maintenance as sweep_pt<2>.
+namespace tsw2 {
+constexpr int TX = 32, TY = 8, HX = TX + 4, HY = TY + 2, HB = 384, FB = TX * TY;
+constexpr size_t SLOT = 2 * HB + 2 * FB;
+constexpr size_t SMEM = 2 * SLOT * 8 + 2 * 8;
+constexpr unsigned TXB = 2u * HX * HY * 8u + 2u * FB * 8u;
+}  // namespace tsw2
+
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map,
+                                          unsigned long long* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"((unsigned long long)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int EA, unsigned MASK>
+__global__ void __launch_bounds__(256) k_sweep_tma2d(const __grid_constant__ CUtensorMap mapH,
+                                                     const __grid_constant__ CUtensorMap mapF,
+                                                     double* __restrict__ P, Lvl L, BcSpec bc,
+                                                     int steps) {
+    using namespace tsw2;
+    constexpr unsigned OPP = MASK ^ 0xFu;
+    extern __shared__ __align__(128) double sm[];
+    unsigned long long* bar = (unsigned long long*)(sm + 2 * SLOT);
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int x0 = blockIdx.x * TX + 1;
+    const int r0 = 1 + blockIdx.y * steps * TY;  // first block row of this CTA
+    const int nst = min(steps, (L.B[0] - r0 + TY) / TY);
+    auto issue = [&](int st, int s) {
+        double* S = sm + s * SLOT;
+        const int y0 = r0 + st * TY;
+        mbar_expect_tx(&bar[s], TXB);
+        int n = 0, j = 0;
+        for (int k = 0; k < 4; ++k) {
+            if ((OPP >> k) & 1u) {
+                tma_load3(S + n * HB, &mapH, &bar[s], OFF + x0 - 2, y0 - 1, k);
+                ++n;
+            } else {
+                tma_load3(S + 2 * HB + j * FB, &mapF, &bar[s], OFF + x0, y0, k);
+                ++j;
+            }
+        }
+    };
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nst > 0) issue(0, 0);
+    }
+    __syncthreads();
+    const int ci = (ty + 1) * HX + tx + 2;
+    for (int st = 0; st < nst; ++st) {
+        const int s = st & 1;
+        if (tid == 0 && st + 1 < nst) issue(st + 1, s ^ 1);
+        mbar_wait(&bar[s], (st >> 1) & 1);
+        const double* S = sm + s * SLOT;
+        int bb[3] = {r0 + st * TY + ty, x0 + tx, 0};
+        if (bb[0] <= L.B[0] && bb[1] <= L.B[1]) {
+            double nv[4];
+            int j = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (!((MASK >> c) & 1u)) continue;
+                const int k0 = c ^ 2, k1 = c ^ 1;
+                const double* h0 = S + oslot<OPP>(k0) * HB;
+                const double* h1 = S + oslot<OPP>(k1) * HB;
+                const bool q0 = (c & 2) != 0, q1 = (c & 1) != 0;
+                // ((E+W)+N)+S  (KER/numpy_backend.py:44)
+                double ns = ad(h0[ci + (q0 ? 0 : HX)], h0[ci - (q0 ? HX : 0)]);
+                ns = ad(ad(ns, h1[ci + (q1 ? 0 : 1)]), h1[ci - (q1 ? 1 : 0)]);
+                nv[c] = ad(ml(L.h2, S[2 * HB + j * FB + tid]), ml(L.b, ns));
+                ++j;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+            const bool bnd = on_boundary<2>(L, bb);
+            const long pl = at<2>(L, 0, bb[0], bb[1], 0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (!((MASK >> c) & 1u)) continue;
+                if (is_wall<2, EA>(L, c, bb)) continue;
+                const long o = pl + (long)c * L.cls;
+                P[o] = nv[c];
+                if (bnd) write_pads<2, EA>(P, L, bc, c, bb, o, nv[c]);
+            }
+        }
+        __syncthreads();  // slot s is refilled by the next step's prefetch
+    }
+}

@@ -166,3 +166,37 @@ def test_fused_sweep_residual_vs_oracle(P, monkeypatch, shape, spec, env):
     assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
     off, rep2 = run_gpu(P, monkeypatch, {**e, "FASMG_FUSE": 0}, shape, "cell", faces, p0, f0, ml, 3)
     assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
+
+
+@pytest.mark.parametrize("shape,loc,spec", [
+    ((256, 256), "cell", "dirichlet"),
+    ((128, 320), "cell", "mixed"),        # x periodic, partial tile along b1
+    ((256, 128), "edge_ew", "lid"),
+    ((128, 256), "edge_ns", "periodic"),
+])
+def test_tma_sweep_2d_vs_oracle(P, monkeypatch, shape, loc, spec):
+    """k_sweep_tma2d forced onto small 2D levels: bitwise vs the oracle."""
+    import oracle as O
+    faces = C.bc_faces(2, spec)
+    ml = 4
+    p0 = C.rand_field(71, shape, loc, 1)
+    f0 = C.rand_field(72, shape, loc, 1)
+    op = O.OField(shape, loc, 1, p0.copy())
+    of = O.OField(shape, loc, 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 2), 1e-30, 2, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    for k, v in {"FASMG_TMA_MIN": 0, "FASMG_MARCH_CHUNK": 3}.items():
+        monkeypatch.setenv(k, str(v))
+    g = P.unit_grid(shape) if shape[0] == shape[1] else \
+        P.GridLevel(0, shape, (0.0, 0.0), tuple(s / shape[-1] for s in shape))
+    L = getattr(P.Location, LOC[loc])
+    p = P.Field(g, L, 1, p0.copy())
+    f = P.Field(g, L, 1, f0.copy())
+    bc = P.BoundaryCondition(2, tuple((nm, P.FaceRule(k, v)) for nm, (k, v) in faces.items()))
+    _, rep = P.solve(p, f, P.OperatorCoeffs(1.0, 0.5), P.FasParams(1e-30, 2, 2, ml),
+                     P.make_plan("x", 2), bc)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(p.data.cpu().numpy().view(np.uint64), op.data.view(np.uint64))
