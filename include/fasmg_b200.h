@@ -99,6 +99,13 @@ int fasmg_prolong_edge0_3d(const double* coarse, const long* cs, double* fine,
 int fasmg_weno_deriv0_2d(double* out, const long* os, const double* q, const long* qs,
                          const double* wind, const long* ws, int ni, int nj, int oi, int oj,
                          double inv_2h, double eps, void* stream);
+/* whole weno3_convect of component `target` in one pass (PKG/weno.py:54-91,
+ * the winds of PKG/weno.py:26-51 evaluated in place): out = interior view
+ * of the result; vel[a] = data pointer of component a (halo g), vst[3a+b]
+ * its strides; ext = target interior extents */
+int fasmg_weno_convect(double* out, const long* os, const double* const* vel, const long* vst,
+                       int dim, int target, int g, const int* ext, double inv_2h, double eps,
+                       void* stream);
 int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const long* qs,
                          const double* wind, const long* ws, int ni, int nj, int nk, int oi,
                          int oj, int ok, double inv_2h, double eps, void* stream);

@@ -68,6 +68,7 @@ _SIGS = {
     "fasmg_stream_wait": "vv",
     "fasmg_device_count": "I",
     "fasmg_gradient_axis": "psp" + "iIi" + "dS",
+    "fasmg_weno_convect": "psVLiiiIddS",
 }
 
 _CT = {

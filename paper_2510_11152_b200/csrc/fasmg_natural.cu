@@ -7,6 +7,8 @@
 // not use them (it runs on the parity-blocked layout, fasmg_engine.cu); they
 // back the field-level API (smooth, residual, restrict, ... on Field
 // objects) and the WENO / staggered operators of the projection drivers.
+#include <string.h>
+
 #include "fasmg_common.cuh"
 #include "fasmg_internal.h"
 
@@ -807,6 +809,80 @@ int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const lon
     LAUNCH(n, (k_weno3<<<nblk(n, TPB), TPB, 0, S(stream)>>>(out, mk(os), q, mk(qs), wind,
                                                             mk(ws), ni, nj, nk, oi, oj, ok,
                                                             inv_2h, eps, p[0], p[1], p[2])));
+}
+
+// Whole weno3_convect of one target component in one pass (PKG/weno.py:
+// 54-91): for every target interior point, sum over derivative axes a of
+// wind_a * weno3(q along a), accumulated from +0.0 in axis order exactly as
+// the reference's per-axis kernel calls on a zeroed array; the wind of a
+// foreign axis is the 4-point average 0.25*((v00+v01)+(v10+v11)) of
+// _avg_to_target (PKG/weno.py:26-51), evaluated in place instead of being
+// materialised.  vel[a]: data pointer + strides of component a (halo g),
+// q = vel[target].  One thread per target interior point.
+struct Vel3 { const double* p[3]; long s[3][3]; int n[3][3]; };
+__global__ void k_weno_convect(double* out, S3 os, Vel3 V, int dim, int target, int g,
+                               int e0, int e1, int e2, double inv_2h, double eps) {
+    const long n = (long)e0 * e1 * (dim == 3 ? e2 : 1);
+    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int I[3];
+    if (dim == 3) {
+        I[2] = (int)(t % e2);
+        const long r = t / e2;
+        I[1] = (int)(r % e1);
+        I[0] = (int)(r / e1);
+    } else {
+        I[2] = 0;
+        I[1] = (int)(t % e1);
+        I[0] = (int)(t / e1);
+    }
+    const double* q = V.p[target];
+    auto Q = [&](int a, int d) {  // q at data index (I + g) shifted by d along a
+        long o = 0;
+        for (int b = 0; b < dim; ++b) o += (long)(I[b] + g + (b == a ? d : 0)) * V.s[target][b];
+        return q[o];
+    };
+    double acc = 0.0;
+    for (int a = 0; a < dim; ++a) {
+        double w;
+        if (a == target) {
+            w = Q(0, 0);
+        } else {
+            // core index of vel[a]: target axis I+1+dt, own axis I+da, else I+1;
+            // data index = core + g - 1
+            auto A = [&](int dt, int da) {
+                long o = 0;
+                for (int b = 0; b < dim; ++b) {
+                    const int c = b == target ? I[b] + 1 + dt : (b == a ? I[b] + da : I[b] + 1);
+                    o += (long)(c + g - 1) * V.s[a][b];
+                }
+                return V.p[a][o];
+            };
+            w = ml(0.25, ad(ad(A(0, 0), A(0, 1)), ad(A(1, 0), A(1, 1))));
+        }
+        const double qm2 = Q(a, -2), qm1 = Q(a, -1), q0 = Q(a, 0), qp1 = Q(a, 1), qp2 = Q(a, 2);
+        const double dm2 = sb(qm1, qm2), dm1 = sb(q0, qm1), dp1 = sb(qp1, q0), dp2 = sb(qp2, qp1);
+        acc = ad(acc, ml(w, weno_point(dm2, dm1, dp1, dp2, w, inv_2h, eps)));
+    }
+    out[I3(os.s, I[0], I[1], I[2])] = acc;
+}
+
+int fasmg_weno_convect(double* out, const long* os, const double* const* vel, const long* vst,
+                       int dim, int target, int g, const int* ext, double inv_2h, double eps,
+                       void* stream) {
+    if (dim != 2 && dim != 3) return fasmg_set_error(FASMG_EINVAL, "dim must be 2 or 3");
+    Vel3 V;
+    memset(&V, 0, sizeof(V));
+    for (int a = 0; a < dim; ++a) {
+        V.p[a] = vel[a];
+        for (int b = 0; b < 3; ++b) V.s[a][b] = b < dim ? vst[3 * a + b] : 0;
+    }
+    S3 o = mk(os);
+    if (dim == 2) o.s[2] = 0;
+    const long n = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
+    LAUNCH(n, (k_weno_convect<<<nblk(n, TPB), TPB, 0, S(stream)>>>(
+                  out, o, V, dim, target, g, ext[0], ext[1], dim == 3 ? ext[2] : 1, inv_2h,
+                  eps)));
 }
 
 // fill_ghosts on a natural-layout C-contiguous data array (PKG/boundary.py:90)

@@ -85,3 +85,23 @@ def test_ns_3d_32_matches_oracle(P, order):
                 assert np.array_equal(got.view(np.uint64), orc.un[c].data.view(np.uint64)), (k, c)
     finally:
         O.set_threads(1)
+
+
+@pytest.mark.parametrize("dim,n", [(2, (24, 16)), (3, (8, 12, 16))])
+def test_weno_fused_equals_per_axis(P, dim, n):
+    """fasmg_weno_convect (one pass, winds in place) is bitwise the
+    reference's per-axis kernel sequence, for every target component."""
+    from paper_2510_11152_b200.weno import weno3_convect
+    g = P.GridLevel(0, n, (0.0,) * dim, tuple(x / n[-1] for x in n))
+    locs = [P.Location.EDGE_EW, P.Location.EDGE_NS, P.Location.EDGE_TB][:dim]
+    rng = np.random.default_rng(dim)
+    vel = []
+    for L in locs:
+        F = P.Field(g, L, 2)
+        F.data.copy_(torch.from_numpy(rng.standard_normal(tuple(F.data.shape))))
+        F.ghosts_fresh = True
+        vel.append(F)
+    for t in range(dim):
+        a = weno3_convect(tuple(vel), t, fused=True).interior.cpu().numpy()
+        b = weno3_convect(tuple(vel), t, fused=False).interior.cpu().numpy()
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), t
