@@ -262,6 +262,75 @@ __device__ __forceinline__ double weno_point(double dm2, double dm1, double dp1,
 // last axis may be the strided one; `fast` names the view axis with the
 // smallest output stride, which consecutive threads walk (coalescing only:
 // every point's arithmetic is unchanged).
+// Whole weno3_convect of one target component in one pass (PKG/weno.py:
+// 54-91): for every target interior point, sum over derivative axes a of
+// wind_a * weno3(q along a), accumulated from +0.0 in axis order exactly as
+// the reference's per-axis kernel calls on a zeroed array; the wind of a
+// foreign axis is the 4-point average 0.25*((v00+v01)+(v10+v11)) of
+// _avg_to_target (PKG/weno.py:26-51), evaluated in place instead of being
+// materialised.  vel[a]: data pointer + strides of component a (halo g),
+// q = vel[target].  One thread per target interior point.
+struct Vel3 { const double* p[3]; long s[3][3]; int n[3][3]; };
+template <int DIM, int TGT>
+__global__ void __launch_bounds__(256) k_weno_convect(double* out, S3 os, Vel3 V, int g, int e0,
+                                                      int e1, int e2, double inv_2h, double eps) {
+    const long n = (long)e0 * e1 * (DIM == 3 ? e2 : 1);
+    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int I[3];
+    if (DIM == 3) {
+        I[2] = (int)(t % e2);
+        const long r = t / e2;
+        I[1] = (int)(r % e1);
+        I[0] = (int)(r / e1);
+    } else {
+        I[2] = 0;
+        I[1] = (int)(t % e1);
+        I[0] = (int)(t / e1);
+    }
+    const double* q = V.p[TGT];
+    long qc = 0;  // q at data index I + g
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) qc += (long)(I[b] + g) * V.s[TGT][b];
+    // every load first (5 q values per axis, 4 wind values per foreign axis),
+    // then the per-axis WENO points (independent), then the ordered sum
+    double qv[DIM][5], w[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) qv[a][d] = q[qc + (long)(d - 2) * V.s[TGT][a]];
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        if (a == TGT) continue;
+        // core index of vel[a]: target axis I+1+dt, own axis I+da, else I+1;
+        // data index = core + g - 1
+        long base = 0;
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) {
+            const int c = b == TGT ? I[b] + 1 : (b == a ? I[b] : I[b] + 1);
+            base += (long)(c + g - 1) * V.s[a][b];
+        }
+        const double* va = V.p[a];
+        const long st = V.s[a][TGT], sa = V.s[a][a];
+        const double v00 = va[base], v01 = va[base + sa], v10 = va[base + st],
+                     v11 = va[base + st + sa];
+        w[a] = ml(0.25, ad(ad(v00, v01), ad(v10, v11)));  // PKG/weno.py:51
+    }
+    w[TGT] = qv[0][2];
+    double term[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const double dm2 = sb(qv[a][1], qv[a][0]), dm1 = sb(qv[a][2], qv[a][1]);
+        const double dp1 = sb(qv[a][3], qv[a][2]), dp2 = sb(qv[a][4], qv[a][3]);
+        term[a] = ml(w[a], weno_point(dm2, dm1, dp1, dp2, w[a], inv_2h, eps));
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) acc = ad(acc, term[a]);
+    out[I3(os.s, I[0], I[1], I[2])] = acc;
+}
+
 __global__ void k_weno2(double* out, S3 os, const double* q, S3 qs, const double* wind, S3 ws,
                         int ni, int nj, int oi, int oj, double inv_2h, double eps, int fast) {
     long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -811,62 +880,6 @@ int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const lon
                                                             inv_2h, eps, p[0], p[1], p[2])));
 }
 
-// Whole weno3_convect of one target component in one pass (PKG/weno.py:
-// 54-91): for every target interior point, sum over derivative axes a of
-// wind_a * weno3(q along a), accumulated from +0.0 in axis order exactly as
-// the reference's per-axis kernel calls on a zeroed array; the wind of a
-// foreign axis is the 4-point average 0.25*((v00+v01)+(v10+v11)) of
-// _avg_to_target (PKG/weno.py:26-51), evaluated in place instead of being
-// materialised.  vel[a]: data pointer + strides of component a (halo g),
-// q = vel[target].  One thread per target interior point.
-struct Vel3 { const double* p[3]; long s[3][3]; int n[3][3]; };
-__global__ void k_weno_convect(double* out, S3 os, Vel3 V, int dim, int target, int g,
-                               int e0, int e1, int e2, double inv_2h, double eps) {
-    const long n = (long)e0 * e1 * (dim == 3 ? e2 : 1);
-    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    int I[3];
-    if (dim == 3) {
-        I[2] = (int)(t % e2);
-        const long r = t / e2;
-        I[1] = (int)(r % e1);
-        I[0] = (int)(r / e1);
-    } else {
-        I[2] = 0;
-        I[1] = (int)(t % e1);
-        I[0] = (int)(t / e1);
-    }
-    const double* q = V.p[target];
-    auto Q = [&](int a, int d) {  // q at data index (I + g) shifted by d along a
-        long o = 0;
-        for (int b = 0; b < dim; ++b) o += (long)(I[b] + g + (b == a ? d : 0)) * V.s[target][b];
-        return q[o];
-    };
-    double acc = 0.0;
-    for (int a = 0; a < dim; ++a) {
-        double w;
-        if (a == target) {
-            w = Q(0, 0);
-        } else {
-            // core index of vel[a]: target axis I+1+dt, own axis I+da, else I+1;
-            // data index = core + g - 1
-            auto A = [&](int dt, int da) {
-                long o = 0;
-                for (int b = 0; b < dim; ++b) {
-                    const int c = b == target ? I[b] + 1 + dt : (b == a ? I[b] + da : I[b] + 1);
-                    o += (long)(c + g - 1) * V.s[a][b];
-                }
-                return V.p[a][o];
-            };
-            w = ml(0.25, ad(ad(A(0, 0), A(0, 1)), ad(A(1, 0), A(1, 1))));
-        }
-        const double qm2 = Q(a, -2), qm1 = Q(a, -1), q0 = Q(a, 0), qp1 = Q(a, 1), qp2 = Q(a, 2);
-        const double dm2 = sb(qm1, qm2), dm1 = sb(q0, qm1), dp1 = sb(qp1, q0), dp2 = sb(qp2, qp1);
-        acc = ad(acc, ml(w, weno_point(dm2, dm1, dp1, dp2, w, inv_2h, eps)));
-    }
-    out[I3(os.s, I[0], I[1], I[2])] = acc;
-}
-
 int fasmg_weno_convect(double* out, const long* os, const double* const* vel, const long* vst,
                        int dim, int target, int g, const int* ext, double inv_2h, double eps,
                        void* stream) {
@@ -880,9 +893,20 @@ int fasmg_weno_convect(double* out, const long* os, const double* const* vel, co
     S3 o = mk(os);
     if (dim == 2) o.s[2] = 0;
     const long n = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
-    LAUNCH(n, (k_weno_convect<<<nblk(n, TPB), TPB, 0, S(stream)>>>(
-                  out, o, V, dim, target, g, ext[0], ext[1], dim == 3 ? ext[2] : 1, inv_2h,
-                  eps)));
+    if (target < 0 || target >= dim) return fasmg_set_error(FASMG_EINVAL, "bad target axis");
+    const int e2 = dim == 3 ? ext[2] : 1;
+    const unsigned nb = nblk(n, TPB);
+    if (n > 0) {
+        if (dim == 2) {
+            if (target == 0) k_weno_convect<2, 0><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            else k_weno_convect<2, 1><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+        } else {
+            if (target == 0) k_weno_convect<3, 0><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            else if (target == 1) k_weno_convect<3, 1><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            else k_weno_convect<3, 2><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+        }
+    }
+    return fasmg_check_launch();
 }
 
 // fill_ghosts on a natural-layout C-contiguous data array (PKG/boundary.py:90)
