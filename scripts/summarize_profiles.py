@@ -34,7 +34,7 @@ for k in sorted(L):
     tot[key][0] += 1
     tot[key][1] += t
     tot[key][2] += by
-    if key.startswith("k_sweep") and t > 0:
+    if key.startswith("k_sweep_tma") and t > 0:
         fine_sweeps.append((t, by))
 alltime = sum(v[1] for v in tot.values())
 out.append(f"# {tag}: ncu launch list of one eager V-cycle + norm, 3D {n}^3 heat "
