@@ -742,6 +742,8 @@ struct Engine {
     bool tma_ok[32] = {};               // level k half-sweeps use k_sweep_tma
     CUtensorMap mapH[32], mapI[32], mapF[32], mapT[32], mapP8[32];
     int resid_tma = 1;                  // FASMG_RESID_TMA: tau / norm on the TMA march
+    int corr_fuse = 1;                  // FASMG_CORR_FUSE: correction fused into the first post half-sweep
+    int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
     // ---- coarse levels in one cluster launch (fasmg_coarse.cuh) ----
     int coarse_k0 = -1;                 // first level run by k_coarse_cycle (-1: none)
     int coarse_cs = 8;                  // FASMG_COARSE_CS: CTAs per cluster
@@ -762,6 +764,19 @@ struct Tile {
 // tau / outer norm of level k on the TMA march (cell-centred, unsharded)
 static bool resid_tma_level(const Engine& E, int k) {
     return E.resid_tma && E.dim == 3 && E.ea < 0 && E.tma_ok[k] && !E.sharded(k);
+}
+
+// level k's coarse correction rides on its first post-smoothing half-sweep
+// (k_sweep_tma<.., CORR>): 3D cell-centred TMA level, unsharded, no periodic
+// face, first two half-sweeps complementary X/RBGS color groups
+static bool corr_fused(const Engine& E, int k) {
+    if (!E.corr_fuse || E.fuse || E.dim != 3 || E.ea >= 0 || !E.tma_ok[k] || E.sharded(k) ||
+        k + 1 >= E.nl || !E.PI[k + 1] || E.masks.size() < 2 || E.wave_T > 0)
+        return false;
+    for (int a = 0; a < 3; ++a)
+        if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
+    const unsigned m0 = E.masks[0], m1 = E.masks[1];
+    return (m0 == 0x96u || m0 == 0x69u) && m1 == (m0 ^ 0xFFu);
 }
 
 static dim3 resid_grid(const Lvl& L, int chunk) {
@@ -1075,10 +1090,28 @@ static bool wave_seq(const Engine& E, int k, std::vector<unsigned>& seq) {
 }
 
 // skip_last: leave the stage's final half-sweep to a fused kernel
+// the first post-smoothing half-sweep of level k with the coarse correction
+// applied on the fly (k_sweep_tma<-1, M, true>; see corr_fused)
+static void launch_sweep_corr(Engine& E, int k, unsigned m) {
+    using namespace tsw;
+    const Lvl& L = E.L[k];
+    const Lvl& Lc = E.L[k + 1];
+    const int chunk = E.corr_chunk > 0 ? E.corr_chunk : (E.march_chunk > 0 ? E.march_chunk : 4);
+    dim3 blk(TX, TY, 1);
+    dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
+    if (m == 0x96u)
+        k_sweep_tma<-1, 0x96u, true><<<grd, blk, SMEM_CORR, E.stream>>>(
+            E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc);
+    else
+        k_sweep_tma<-1, 0x69u, true><<<grd, blk, SMEM_CORR, E.stream>>>(
+            E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc);
+}
+
 template <int D>
-static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false) {
+static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false,
+                          bool first_corr = false) {
     std::vector<unsigned> seq;
-    if (D == 3 && wave_seq(E, k, seq)) {
+    if (D == 3 && !first_corr && wave_seq(E, k, seq)) {
         const int n = (int)seq.size() - (skip_last ? 1 : 0);
         for (int i = 0; i < n; i += E.wave_T) launch_wave(E, k, seq, i, std::min(E.wave_T, n - i), cnt);
         return;
@@ -1089,7 +1122,12 @@ static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false) {
     for (int it = 0; it < E.s; ++it)
         for (unsigned m : E.masks) {
             if (skip_last && ++done == total) return;
-            EA_DISPATCH(D, E.ea, (sweep_mask<D, EA>(E, k, m, t)));
+            if (first_corr && it == 0 && m == E.masks[0] && done <= 1) {
+                launch_sweep_corr(E, k, m);
+                first_corr = false;
+            } else {
+                EA_DISPATCH(D, E.ea, (sweep_mask<D, EA>(E, k, m, t)));
+            }
             ++cnt;
             halo_exchange<D>(E, k, m, cnt);
         }
@@ -1180,11 +1218,12 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
                     const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
                     k_resid_tma<1><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
                                      E.stream>>>(E.mapT[k], E.mapP8[k], E.F[k], L, E.bc, ch,
-                                                 nullptr, E.P[k + 1], E.F[k + 1], Lc);
+                                                 nullptr, E.P[k + 1], E.F[k + 1], Lc,
+                                                 corr_fused(E, k) ? E.PI[k + 1] : nullptr);
                 } else {
-                    k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L,
-                                                                     E.P[k + 1], E.F[k + 1], Lc,
-                                                                     E.bc);
+                    k_tau_fast<D><<<t.grid, t.block, 0, E.stream>>>(
+                        E.P[k], E.F[k], L, E.P[k + 1], E.F[k + 1], Lc, E.bc,
+                        corr_fused(E, k) ? E.PI[k + 1] : nullptr);
                 }
                 ++cnt;
             }
@@ -1227,9 +1266,13 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L);
+        const bool cf = D == 3 && corr_fused(E, k);  // correction rides on the first sweep
         if (E.ea < 0) {
-            k_correct_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc, E.bc);
-            ++cnt;
+            if (!cf) {
+                k_correct_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc,
+                                                                     E.bc);
+                ++cnt;
+            }
         } else {
             if (E.edge_fast) {
                 const long tot = Lc.cls * (1L << D);
@@ -1248,10 +1291,10 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
         }
         halo_exchange<D>(E, k, ALL, cnt);
         if (k == 0 && fuse_norm) {
-            launch_smooth<D>(E, k, cnt, true);
+            launch_smooth<D>(E, k, cnt, true, cf);
             launch_fused<fsw::MODE_NORM>(E, k, cnt);
         } else {
-            launch_smooth<D>(E, k, cnt);
+            launch_smooth<D>(E, k, cnt, false, cf);
         }
     }
 }
@@ -1271,7 +1314,7 @@ static void launch_norm(Engine& E, long& cnt, bool fused = false) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
             k_resid_tma<0><<<g, dim3(rsw::TX, rsw::TY, 1), rsw::SMEM, E.stream>>>(
-                E.mapT[0], E.mapP8[0], E.F[0], L, E.bc, ch, E.part, nullptr, nullptr, L);
+                E.mapT[0], E.mapP8[0], E.F[0], L, E.bc, ch, E.part, nullptr, nullptr, L, nullptr);
             npart_norm = (int)(g.x * g.y * g.z);
         } else if (E.ea < 0) {
             // (walking axis 0 in chunks per thread measured slower: 1 block)
@@ -1391,6 +1434,12 @@ static int tma_attr() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_sweep_tma<EA, 0x69u>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess && EA == -1)
+        e = cudaFuncSetAttribute(k_sweep_tma<-1, 0x96u, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsw::SMEM_CORR);
+    if (e == cudaSuccess && EA == -1)
+        e = cudaFuncSetAttribute(k_sweep_tma<-1, 0x69u, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsw::SMEM_CORR);
     return fasmg_check(e);
 }
 
@@ -1436,6 +1485,8 @@ static int tma_setup(Engine& E) {
     }
     if (!any) return 0;
     if (const char* v = getenv("FASMG_RESID_TMA")) E.resid_tma = atoi(v);
+    if (const char* v = getenv("FASMG_CORR_FUSE")) E.corr_fuse = atoi(v);
+    if (const char* v = getenv("FASMG_CORR_CHUNK")) E.corr_chunk = atoi(v);
     int st = 0;
     EA_DISPATCH(3, E.ea, (st = tma_attr<EA>()));
     if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<0>,
@@ -1698,6 +1749,10 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         }
         cudaMemsetAsync(E->P[k], 0, bytes, E->stream);
         cudaMemsetAsync(E->F[k], 0, bytes, E->stream);
+        if (ea < 0 && dim == 3 && nranks == 1 && k >= 1) {  // pinit for the fused correction
+            if (fasmg_check(cudaMalloc(&E->PI[k], bytes))) { delete E; return nullptr; }
+            cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
+        }
         if (ea >= 0) {
             if (fasmg_check(cudaMalloc(&E->R[k], bytes))) { delete E; return nullptr; }
             if (k >= 1 && fasmg_check(cudaMalloc(&E->PI[k], bytes))) { delete E; return nullptr; }

@@ -582,7 +582,7 @@ template <int D>
 __device__ __forceinline__ void tau_pt(const double* __restrict__ P, const double* __restrict__ F,
                                        const Lvl& L, double* __restrict__ Pc,
                                        double* __restrict__ Fc, const Lvl& Lc, const BcSpec& bc,
-                                       const int* bb) {
+                                       const int* bb, double* __restrict__ PIc = nullptr) {
     constexpr int NC = 1 << D;
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
     // phase 1: all loads (2^d centers, 2^d f, and the d*2^(d-1) neighbors
@@ -627,6 +627,7 @@ __device__ __forceinline__ void tau_pt(const double* __restrict__ P, const doubl
     const long oc = at<D>(Lc, cc, cb[0], cb[1], cb[2]);
     const double pcv = ml(rp, sc);
     Pc[oc] = pcv;
+    if (PIc) PIc[oc] = pcv;  // pinit, for the fused correction
     Fc[oc] = ml(rr, sc);
     if (on_boundary<D>(Lc, cb)) write_pads<D, -1>(Pc, Lc, bc, cc, cb, oc, pcv);
 }
@@ -635,10 +636,11 @@ template <int D>
 __global__ void __launch_bounds__(256) k_tau_fast(const double* __restrict__ P,
                                                   const double* __restrict__ F, Lvl L,
                                                   double* __restrict__ Pc,
-                                                  double* __restrict__ Fc, Lvl Lc, BcSpec bc) {
+                                                  double* __restrict__ Fc, Lvl Lc, BcSpec bc,
+                                                  double* __restrict__ PIc = nullptr) {
     int bb[3];
     if (!tile_coords<D>(L, bb)) return;
-    tau_pt<D>(P, F, L, Pc, Fc, Lc, bc, bb);
+    tau_pt<D>(P, F, L, Pc, Fc, Lc, bc, bb, PIc);
 }
 
 // f_c += a*p_c - b*Lap(p_c) on the coarse level (PKG/fas.py:108-110)

@@ -339,20 +339,38 @@ constexpr int HB = 384;        // doubles per halo box slot (360 -> 128 B multip
 constexpr int FB = TX * TY;    // f box
 constexpr int RING = 3;
 constexpr unsigned HBYTES = HX * HY * 8u, FBYTES = FB * 8u;
+constexpr int CX = TX + 2, CY = TY + 2, CB = CX * CY;  // corr tile (block ring)
+constexpr int CRING = 4;
 constexpr size_t SMEM = (size_t)(4 * RING * HB + 2 * 4 * FB) * 8 + 2 * 8;
+constexpr size_t SMEM_CORR = SMEM + (size_t)CRING * CB * 8;
 }  // namespace tsw
 
-template <int EA, unsigned MASK>
+// CORR: this is the FIRST post-smoothing half-sweep of the level and also
+// applies the coarse correction (PKG/fas.py:119-124) on the fly -- the
+// prolongation+correction fused into the first post-smoothing color.  The
+// correction of fine block b is corr = p_c - pinit at its coarse cell (pinit
+// = R(p) stored by the tau pass, bitwise what the reference stores).  Every
+// opposite-color (B) neighbour is read as B + corr(its block); a boundary
+// point's own ghost is rebuilt from its corrected value (the stored ghost
+// predates the correction); the tile's B values stay uncorrected in memory
+// -- the next half-sweep overwrites them without reading them -- but their
+// ghost pads are written from the corrected values.  Because no CTA
+// modifies a B value, neighbours read consistent data (no cross-CTA race).
+// Requires: cell-centred, no periodic face, next half-sweep = the other color.
+template <int EA, unsigned MASK, bool CORR = false>
 __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUtensorMap mapH,
                                                    const __grid_constant__ CUtensorMap mapF,
                                                    double* __restrict__ P, Lvl L, BcSpec bc,
-                                                   int chunk) {
+                                                   int chunk, const double* __restrict__ Pc = nullptr,
+                                                   const double* __restrict__ PIc = nullptr,
+                                                   Lvl Lc = Lvl()) {
     using namespace tsw;
     constexpr unsigned OPP = MASK ^ 0xFFu;
     extern __shared__ __align__(128) double sm[];
     double* opp = sm;                        // [4][RING][HB]
     double* fsm = sm + 4 * RING * HB;        // [2][4][FB]
     unsigned long long* bar = (unsigned long long*)(fsm + 2 * 4 * FB);
+    double* csm = (double*)(bar + 2);        // (CORR) [CRING][CB] corrections, planes b0-1..b0+2
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int x0 = blockIdx.x * TX + 1, y0 = blockIdx.y * TY + 1;
     const int b0s = 1 + blockIdx.z * chunk;
@@ -361,6 +379,41 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
     bb[2] = x0 + tx;
     bb[1] = y0 + ty;
     const bool active = bb[1] <= L.B[1] && bb[2] <= L.B[2];
+    // (CORR) corrections p_c - pinit (PKG/fas.py:119) of a plane's corr tile:
+    // block (y0-1+r, x0-1+q) at entry r*CX+q; thread tid covers entries tid
+    // and tid+256.  corr_fetch only issues the loads (v: Pc, pinit pairs);
+    // corr_store subtracts and stores -- a step later, so the latency hides.
+    auto corr_fetch = [&](int pl, double* v) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int e = tid + i * 256;
+            const int b1 = y0 - 1 + e / CX, b2 = x0 - 1 + e % CX;
+            v[2 * i] = v[2 * i + 1] = 0.0;
+            if (e < CB && pl >= 1 && pl <= L.B[0] && b1 >= 1 && b1 <= L.B[1] && b2 >= 1 &&
+                b2 <= L.B[2]) {
+                int fb[3] = {pl, b1, b2}, cc = 0, cb[3] = {0, 0, 0};
+                coarse_of<3>(L, Lc, fb, cc, cb);
+                const long oc = at<3>(Lc, cc, cb[0], cb[1], cb[2]);
+                v[2 * i] = __ldg(Pc + oc);
+                v[2 * i + 1] = __ldg(PIc + oc);
+            }
+        }
+    };
+    auto corr_store = [&](int pl, const double* v) {
+        double* d = csm + ((pl + CRING) % CRING) * CB;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int e = tid + i * 256;
+            if (e < CB) d[e] = sb(v[2 * i], v[2 * i + 1]);
+        }
+    };
+    if (CORR) {  // prologue: planes b0s-1, b0s, b0s+1 (all loads in flight at once)
+        double v[3][4];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) corr_fetch(b0s - 1 + i, v[i]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) corr_store(b0s - 1 + i, v[i]);
+    }
 
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -402,9 +455,37 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 }
             }
         }
+        bb[0] = b0;
+        const long pl = col + (long)b0 * L.s0;
+        const int Bn[3] = {L.G0, L.B[1], L.B[2]};
+        // (CORR) prefetch the corrections of plane b0+2 (stored at the end of
+        // the step); this step's come from the shared ring
+        double cpre[4] = {0.0, 0.0, 0.0, 0.0};
+        if (CORR) corr_fetch(b0 + 2, cpre);
+        double c_own = 0.0, cW[3] = {0.0, 0.0, 0.0}, cE[3] = {0.0, 0.0, 0.0};
+        double araw[8];
+        if (CORR && active) {
+            const int cc0 = (ty + 1) * CX + tx + 1;
+            const double* cp = csm + ((b0 + CRING) % CRING) * CB;
+            c_own = cp[cc0];
+            cW[0] = csm[((b0 - 1 + CRING) % CRING) * CB + cc0];
+            cE[0] = csm[((b0 + 1) % CRING) * CB + cc0];
+            cW[1] = cp[cc0 - CX];
+            cE[1] = cp[cc0 + CX];
+            cW[2] = cp[cc0 - 1];
+            cE[2] = cp[cc0 + 1];
+            // a point's own value is only needed for its ghost (boundary)
+            if (on_boundary<3>(L, bb)) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if ((MASK >> c) & 1u) araw[c] = __ldg(P + pl + (long)c * L.cls);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) araw[c] = 0.0;
+            }
+        }
         mbar_wait(&bar[b0 & 1], ((b0 - b0s) >> 1) & 1);
         if (active) {
-            bb[0] = b0;
             const int ci = (ty + 1) * HX + tx + 2;  // tile centre in a halo box
             double nv[8];
             int j = 0;
@@ -414,18 +495,31 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 const int k0 = c ^ 4, k1 = c ^ 2, k2 = c ^ 1;
                 const int lo0 = (k0 & 4) ? b0 : b0 - 1;
                 const double* w0 = opp + oslot<OPP>(k0) * RING * HB;
+                const double* wy = opp + (oslot<OPP>(k1) * RING + (b0 % RING)) * HB;
+                const double* wz = opp + (oslot<OPP>(k2) * RING + (b0 % RING)) * HB;
+                const bool q0 = (c & 4) != 0, q1 = (c & 2) != 0, q2 = (c & 1) != 0;
+                double e0 = w0[((lo0 + 1) % RING) * HB + ci], w0v = w0[(lo0 % RING) * HB + ci];
+                double e1 = wy[ci + (q1 ? 0 : HX)], w1 = wy[ci - (q1 ? HX : 0)];
+                double e2 = wz[ci + (q2 ? 0 : 1)], w2 = wz[ci - (q2 ? 1 : 0)];
+                if (CORR) {
+                    // inside the block: own correction; across a face: the
+                    // neighbour block's, or (domain face) the own ghost
+                    const double ac = ad(araw[c], c_own);  // corrected value of this point
+                    auto gh = [&](int a, int sd) {
+                        return bc.kind[a][sd] == BC_DIRICHLET ? sb(ml(2.0, bc.val[a][sd]), ac) : ac;
+                    };
+                    const int g0 = gb0(L, bb);
+                    if (q0) { e0 = ad(e0, c_own); w0v = g0 == 1 ? gh(0, 0) : ad(w0v, cW[0]); }
+                    else { w0v = ad(w0v, c_own); e0 = g0 == Bn[0] ? gh(0, 1) : ad(e0, cE[0]); }
+                    if (q1) { e1 = ad(e1, c_own); w1 = bb[1] == 1 ? gh(1, 0) : ad(w1, cW[1]); }
+                    else { w1 = ad(w1, c_own); e1 = bb[1] == Bn[1] ? gh(1, 1) : ad(e1, cE[1]); }
+                    if (q2) { e2 = ad(e2, c_own); w2 = bb[2] == 1 ? gh(2, 0) : ad(w2, cW[2]); }
+                    else { w2 = ad(w2, c_own); e2 = bb[2] == Bn[2] ? gh(2, 1) : ad(e2, cE[2]); }
+                }
                 // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:62)
-                double ns = ad(w0[((lo0 + 1) % RING) * HB + ci], w0[(lo0 % RING) * HB + ci]);
-                {
-                    const double* w = opp + (oslot<OPP>(k1) * RING + (b0 % RING)) * HB;
-                    const bool q = (c & 2) != 0;
-                    ns = ad(ad(ns, w[ci + (q ? 0 : HX)]), w[ci - (q ? HX : 0)]);
-                }
-                {
-                    const double* w = opp + (oslot<OPP>(k2) * RING + (b0 % RING)) * HB;
-                    const bool q = (c & 1) != 0;
-                    ns = ad(ad(ns, w[ci + (q ? 0 : 1)]), w[ci - (q ? 1 : 0)]);
-                }
+                double ns = ad(e0, w0v);
+                ns = ad(ad(ns, e1), w1);
+                ns = ad(ad(ns, e2), w2);
                 nv[c] = ad(ml(L.h2, fsm[((b0 & 1) * 4 + j) * FB + tid]), ml(L.b, ns));
                 ++j;
             }
@@ -433,7 +527,6 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
             for (int c = 0; c < 8; ++c)
                 if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
             const bool bnd = on_boundary<3>(L, bb);
-            const long pl = col + (long)b0 * L.s0;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (!((MASK >> c) & 1u)) continue;
@@ -442,7 +535,16 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 P[o] = nv[c];
                 if (bnd) write_pads<3, EA>(P, L, bc, c, bb, o, nv[c]);
             }
+            if (CORR && bnd) {  // ghosts of the (uncorrected in memory) B points
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (!((OPP >> k) & 1u)) continue;
+                    const double braw = opp[(oslot<OPP>(k) * RING + (b0 % RING)) * HB + ci];
+                    write_pads<3, EA>(P, L, bc, k, bb, pl + (long)k * L.cls, ad(braw, c_own));
+                }
+            }
         }
+        if (CORR) corr_store(b0 + 2, cpre);  // ring slot of plane b0-2: unused from now on
         __syncthreads();  // the next prefetch overwrites this step's oldest slots
     }
 }
@@ -470,7 +572,8 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                                                    BcSpec bc, int chunk,
                                                    double* __restrict__ part,
                                                    double* __restrict__ Pc,
-                                                   double* __restrict__ Fc, Lvl Lc) {
+                                                   double* __restrict__ Fc, Lvl Lc,
+                                                   double* __restrict__ PIc) {
     using namespace rsw;
     extern __shared__ __align__(128) double sm[];
     unsigned long long* bar = (unsigned long long*)(sm + 2 * SLOT);
@@ -547,6 +650,7 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                 const long oc = at<3>(Lc, cc, cb[0], cb[1], cb[2]);
                 const double pcv = ml(rp, 0.125);
                 Pc[oc] = pcv;
+                if (PIc) PIc[oc] = pcv;  // pinit, for the fused correction
                 Fc[oc] = ml(rr, 0.125);
                 if (on_boundary<3>(Lc, cb)) write_pads<3, -1>(Pc, Lc, bc, cc, cb, oc, pcv);
             }

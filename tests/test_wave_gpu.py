@@ -160,7 +160,7 @@ def test_fused_sweep_residual_vs_oracle(P, monkeypatch, shape, spec, env):
     it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 3, 2, ml,
                            dmin=0.0, dmax=shape[0] / shape[-1])
     O.set_threads(1)
-    e = {"FASMG_TMA_MIN": 0, **env}
+    e = {"FASMG_TMA_MIN": 0, "FASMG_FUSE": 3, **env}
     got, rep = run_gpu(P, monkeypatch, e, shape, "cell", faces, p0, f0, ml, 3)
     np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
     assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
@@ -200,3 +200,47 @@ def test_tma_sweep_2d_vs_oracle(P, monkeypatch, shape, loc, spec):
     torch.cuda.synchronize()
     np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
     assert np.array_equal(p.data.cpu().numpy().view(np.uint64), op.data.view(np.uint64))
+
+
+@pytest.mark.parametrize("shape,spec,env", [
+    ((64, 64, 64), "dirichlet", {}),
+    ((48, 112, 80), "mixed_dn", {}),
+    ((96, 64, 128), "mixed_dn", {"FASMG_MARCH_CHUNK": 5}),
+    ((64, 64, 64), "lid", {"FASMG_MARCH_CHUNK": 1}),
+    ((64, 64, 64), "neumann", {}),
+])
+def test_fused_correction_vs_oracle(P, monkeypatch, shape, spec, env):
+    """Coarse correction fused into the first post-smoothing half-sweep
+    (k_sweep_tma<.., CORR>, pinit stored by the tau pass), forced onto small
+    levels: fields bitwise equal to the oracle and to the unfused path."""
+    import oracle as O
+    faces = faces_of(spec) if spec in FACES else C.bc_faces(3, spec)
+    a = 0.0 if spec == "neumann" else 1.0
+    ml = 3
+    p0 = C.rand_field(81, shape, "cell", 1)
+    f0 = C.rand_field(82, shape, "cell", 1)
+    op = O.OField(shape, "cell", 1, p0.copy())
+    of = O.OField(shape, "cell", 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, a, 0.5, faces, O.plan_colors("x", 3), 1e-30, 3, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    e = {"FASMG_TMA_MIN": 0, **env}
+    got, rep = run_gpu_a(P, monkeypatch, e, shape, faces, p0, f0, ml, 3, a)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+    off, _ = run_gpu_a(P, monkeypatch, {**e, "FASMG_CORR_FUSE": 0}, shape, faces, p0, f0, ml, 3, a)
+    assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
+
+
+def run_gpu_a(P, monkeypatch, env, shape, faces, p0, f0, ml, k_max, a):
+    for k, v in env.items():
+        monkeypatch.setenv(k, str(v))
+    g = P.unit_grid(shape) if len(set(shape)) == 1 else \
+        P.GridLevel(0, shape, (0.0,) * 3, tuple(s / shape[-1] for s in shape))
+    p = P.Field(g, P.Location.CELL, 1, p0.copy())
+    f = P.Field(g, P.Location.CELL, 1, f0.copy())
+    _, rep = P.solve(p, f, P.OperatorCoeffs(a, 0.5), P.FasParams(1e-30, k_max, 2, ml),
+                     P.make_plan("x", 3), bc_of(P, faces))
+    torch.cuda.synchronize()
+    return p.data.cpu().numpy(), rep
