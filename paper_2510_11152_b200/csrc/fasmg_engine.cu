@@ -500,12 +500,15 @@ template <int D, int EA>
 __global__ void __launch_bounds__(TPB) k_correct_edge_fast(double* __restrict__ P, Lvl L,
                                                            const double* __restrict__ Corr,
                                                            Lvl Lc) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= L.nblk) return;
     int bb[3];
-    decode<D>(L, t, bb);
+    if (!tile_coords<D>(L, bb)) return;  // 2D/3D thread tile: no 64-bit div/mod
     constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = D == 3 ? (P0 == 2 ? 1 : 2) : 0;
     const int be = bb[P0], bj = bb[P1], bk = D == 3 ? bb[P2] : 0;
+    // the block's fine values first (independent of the coarse loads below)
+    const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+    double pv[1 << D];
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) pv[c] = P[o0 + (long)c * L.cls];
     BlkReader<D> rd{Corr, Lc};
     double cv[2][3][3];
 #pragma unroll
@@ -533,8 +536,7 @@ __global__ void __launch_bounds__(TPB) k_correct_edge_fast(double* __restrict__ 
             return ml(ad(ml(3.0, t_near), t_far), 0.25);
         };
         const double v = qe ? ml(ad(line(0), line(1)), 0.5) : line(1);
-        const long o = at<D>(L, c, bb[0], bb[1], bb[2]);
-        P[o] = ad(P[o], v);
+        P[o0 + (long)c * L.cls] = ad(pv[c], v);
     }
 }
 
@@ -1278,7 +1280,7 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
                 const long tot = Lc.cls * (1L << D);
                 k_corr_edge<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc,
                                                                    E.bch, E.R[k + 1]);
-                EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<nb(L.nblk, TPB), TPB, 0,
+                EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<t.grid, t.block, 0,
                                                                    E.stream>>>(E.P[k], L,
                                                                                E.R[k + 1], Lc)));
                 cnt += 2;
@@ -1310,11 +1312,13 @@ static void launch_norm(Engine& E, long& cnt, bool fused = false) {
     const Tile t = tile_of(L);
     int npart_norm = E.npart;
     if (!fused) {
-        if (D == 3 && resid_tma_level(E, 0)) {
+        if (D == 3 && E.resid_tma && E.tma_ok[0] && !E.sharded(0)) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
-            k_resid_tma<0><<<g, dim3(rsw::TX, rsw::TY, 1), rsw::SMEM, E.stream>>>(
-                E.mapT[0], E.mapP8[0], E.F[0], L, E.bc, ch, E.part, nullptr, nullptr, L, nullptr);
+            EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA><<<g, dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
+                                                       E.stream>>>(
+                                     E.mapT[0], E.mapP8[0], E.F[0], L, E.bc, ch, E.part, nullptr,
+                                     nullptr, L, nullptr)));
             npart_norm = (int)(g.x * g.y * g.z);
         } else if (E.ea < 0) {
             // (walking axis 0 in chunks per thread measured slower: 1 block)
@@ -1489,9 +1493,10 @@ static int tma_setup(Engine& E) {
     if (const char* v = getenv("FASMG_CORR_CHUNK")) E.corr_chunk = atoi(v);
     int st = 0;
     EA_DISPATCH(3, E.ea, (st = tma_attr<EA>()));
-    if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<0>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)rsw::SMEM));
+    if (!st) EA_DISPATCH(3, E.ea, (st = fasmg_check(cudaFuncSetAttribute(
+                                        k_resid_tma<0, EA>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)rsw::SMEM))));
     if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)rsw::SMEM));

@@ -565,7 +565,7 @@ constexpr size_t SMEM = 2 * SLOT * 8 + 2 * 8;
 constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u + 8u * IB * 8u;
 }  // namespace rsw
 
-template <int MODE>
+template <int MODE, int EA = -1>
 __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUtensorMap mapH,
                                                    const __grid_constant__ CUtensorMap mapI,
                                                    const double* __restrict__ F, Lvl L,
@@ -638,7 +638,9 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                 const double lap = ml(sb(ns, ml(6.0, pc[c])), L.inv_h2);
                 const double r = sb(fv[c], sb(ml(L.a, pc[c]), ml(L.b, lap)));
                 if (MODE == 0) {
-                    acc = ad(acc, ml(r, r));
+                    // edge fields: wall points are not unknowns (PKG/grid.py:199-208)
+                    int bw[3] = {b0, b1, b2};
+                    if (!is_wall<3, EA>(L, c, bw)) acc = ad(acc, ml(r, r));
                 } else {
                     if (c == 7) { rp = pc[c]; rr = r; }
                     else { rp = ad(rp, pc[c]); rr = ad(rr, r); }
