@@ -1219,7 +1219,7 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
                 if (D == 3 && resid_tma_level(E, k)) {
                     const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
                     k_resid_tma<1><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
-                                     E.stream>>>(E.mapT[k], E.mapP8[k], E.F[k], L, E.bc, ch,
+                                     E.stream>>>(E.mapT[k], E.P[k], E.F[k], L, E.bc, ch,
                                                  nullptr, E.P[k + 1], E.F[k + 1], Lc,
                                                  corr_fused(E, k) ? E.PI[k + 1] : nullptr);
                 } else {
@@ -1317,7 +1317,7 @@ static void launch_norm(Engine& E, long& cnt, bool fused = false) {
             const dim3 g = resid_grid(L, ch);
             EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA><<<g, dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
                                                        E.stream>>>(
-                                     E.mapT[0], E.mapP8[0], E.F[0], L, E.bc, ch, E.part, nullptr,
+                                     E.mapT[0], E.P[0], E.F[0], L, E.bc, ch, E.part, nullptr,
                                      nullptr, L, nullptr)));
             npart_norm = (int)(g.x * g.y * g.z);
         } else if (E.ea < 0) {

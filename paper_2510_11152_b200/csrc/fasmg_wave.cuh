@@ -552,22 +552,23 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
 // ---------------------------------------------------------------------------
 // Residual of a cell-centred level on the same TMA march (k_sweep_tma's
 // tile/chunk geometry): per plane step one thread issues, for each of the
-// 8 classes, the plane-b0 tile with its in-plane halo (36 x 10), the one
-// axis-0 neighbour plane the opposite-q0 classes need (32 x 8, b0+1 for
-// q0=1 classes, b0-1 for q0=0), double-buffered on two mbarriers; f is
-// read straight from global (issued before the barrier wait).  MODE 0 accumulates sum(r^2) (outer norm, PKG/fas.py:149-151;
+// 8 classes, the plane-b0 tile with its in-plane halo (36 x 10) by TMA,
+// double-buffered on two mbarriers; f and the one axis-0 neighbour each
+// class needs (b0+1 for q0=1 classes, b0-1 for q0=0 -- L2 hits, that plane
+// is a neighbouring step's TMA box) are read straight from global, issued
+// before the barrier wait.  40 KB of shared memory per CTA: 4 CTAs per SM.  MODE 0 accumulates sum(r^2) (outer norm, PKG/fas.py:149-151;
 // per-CTA fixed-order partials); MODE 1 restricts r and p into the coarse
 // level (tau pass, PKG/fas.py:99-107) with tau_pt's exact arithmetic.
 namespace rsw {
 constexpr int TX = 32, TY = 8, HX = TX + 4, HB = 384, IB = TX * TY;
-constexpr size_t SLOT = (size_t)8 * HB + 8 * IB;  // halo boxes + axis-0 neighbour boxes
+constexpr size_t SLOT = (size_t)8 * HB;  // halo boxes (axis-0 neighbours: direct loads)
 constexpr size_t SMEM = 2 * SLOT * 8 + 2 * 8;
-constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u + 8u * IB * 8u;
+constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u;
 }  // namespace rsw
 
 template <int MODE, int EA = -1>
 __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUtensorMap mapH,
-                                                   const __grid_constant__ CUtensorMap mapI,
+                                                   const double* __restrict__ P,
                                                    const double* __restrict__ F, Lvl L,
                                                    BcSpec bc, int chunk,
                                                    double* __restrict__ part,
@@ -584,11 +585,8 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
     auto issue = [&](int b0, int s) {
         double* S = sm + s * SLOT;
         mbar_expect_tx(&bar[s], TXB);
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; ++k)
             tma_load4(S + k * HB, &mapH, &bar[s], OFF + x0 - 2, y0 - 1, b0, k);
-            tma_load4(S + 8 * HB + k * IB, &mapI, &bar[s], OFF + x0, y0, (k & 4) ? b0 + 1 : b0 - 1,
-                      k);
-        }
     };
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -604,11 +602,16 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
     for (int b0 = b0s; b0 <= b0e; ++b0) {
         const int s = (b0 - b0s) & 1;
         if (tid == 0 && b0 < b0e) issue(b0 + 1, s ^ 1);
-        double fv[8];
+        // f and the axis-0 neighbour plane of every class straight from global
+        // (coalesced rows, L2-resident), issued before the barrier wait
+        double fv[8], nb0[8];
         if (active) {
             const long o = at<3>(L, 0, b0, b1, b2);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) fv[c] = __ldg(F + o + (long)c * L.cls);
+            for (int c = 0; c < 8; ++c) {
+                fv[c] = __ldg(F + o + (long)c * L.cls);
+                nb0[c] = P[o + (long)c * L.cls + ((c & 4) ? L.s0 : -L.s0)];
+            }
         }
         mbar_wait(&bar[s], ((b0 - b0s) >> 1) & 1);
         const double* S = sm + s * SLOT;
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                     const double inside = pc[k];
                     // across the block face: W of q=1, E of q=0
                     double out;
-                    if (a == 0) out = S[8 * HB + k * IB + tid];
+                    if (a == 0) out = nb0[k];
                     else if (a == 1) out = S[k * HB + ci + (qa ? -HX : HX)];
                     else out = S[k * HB + ci + (qa ? -1 : 1)];
                     const double e = qa ? inside : out;
