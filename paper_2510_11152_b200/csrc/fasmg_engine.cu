@@ -746,6 +746,7 @@ struct Engine {
     int resid_tma = 1;                  // FASMG_RESID_TMA: tau / norm on the TMA march
     int corr_fuse = 1;                  // FASMG_CORR_FUSE: correction fused into the first post half-sweep
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
+    int fuse_push = 1;                  // FASMG_FUSE_PUSH: sweeps store boundary planes into peers' halos
     // ---- coarse levels in one cluster launch (fasmg_coarse.cuh) ----
     int coarse_k0 = -1;                 // first level run by k_coarse_cycle (-1: none)
     int coarse_cs = 8;                  // FASMG_COARSE_CS: CTAs per cluster
@@ -822,9 +823,21 @@ static bool mask_supported(int dim, unsigned m) {
     return m != 0 && (m & (m - 1)) == 0 && m < (1u << (1 << dim));
 }
 
+// the neighbours' halo planes for a fused push (sharded levels only)
+static PeerHalo peer_halo(const Engine& E, int k) {
+    PeerHalo ph;
+    if (!E.fuse_push || !E.sharded(k)) return ph;
+    if (E.rank > 0) ph.lo = E.peers[E.rank - 1].P[k];
+    if (E.rank + 1 < E.nranks) ph.hi = E.peers[E.rank + 1].P[k];
+    return ph;
+}
+
+// returns true when the kernel also pushed the updated boundary planes
 template <int D, int EA, unsigned M>
-static void sweep_one(Engine& E, int k, const Tile& t) {
+static bool sweep_one(Engine& E, int k, const Tile& t) {
     const Lvl& L = E.L[k];
+    const PeerHalo ph = peer_halo(E, k);
+    const bool fused = ph.lo || ph.hi;
     if (E.sweep_variant == 1) {
         constexpr int NCM = __builtin_popcount(M);
         dim3 blk, grd;
@@ -840,7 +853,7 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
             grd = dim3((L.B[1] + bx - 1) / bx, (L.B[0] + by - 1) / by, NCM);
         }
         k_sweep_pc<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
-        return;
+        return false;
     }
     if (E.sweep_variant == 2 && __builtin_popcount(M) > 1) {
         const int chunk = E.march_chunk > 0 ? E.march_chunk : 16;
@@ -857,7 +870,7 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
             grd = dim3((L.B[1] + bx - 1) / bx, nch, 1);
         }
         k_sweep_march<D, EA, M><<<grd, blk, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
-        return;
+        return false;
     }
     if (D == 2 && E.sweep_variant == 4 && E.tma_ok[k] && __builtin_popcount(M) > 1) {
         using namespace tsw2;
@@ -865,8 +878,8 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         dim3 blk(TX, TY, 1);
         dim3 grd((L.B[1] + TX - 1) / TX, (L.B[0] + steps * TY - 1) / (steps * TY), 1);
         k_sweep_tma2d<EA, M><<<grd, blk, SMEM, E.stream>>>(E.mapT[k], E.mapF[k], E.P[k], L,
-                                                           E.bc, steps);
-        return;
+                                                           E.bc, steps, ph);
+        return fused;
     }
     if (D == 3 && E.sweep_variant == 4 && E.tma_ok[k] && __builtin_popcount(M) > 1) {
         using namespace tsw;
@@ -879,8 +892,8 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         dim3 blk(TX, TY, 1);
         dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
         k_sweep_tma<EA, M><<<grd, blk, SMEM, E.stream>>>(E.mapT[k], E.mapF[k], E.P[k], L, E.bc,
-                                                         chunk);
-        return;
+                                                         chunk, nullptr, nullptr, Lvl(), ph);
+        return fused;
     }
     if (D == 3 && E.sweep_variant >= 3 && __builtin_popcount(M) > 1 && L.B[2] >= 32 &&
         L.B[1] >= 8 && L.nblk >= (1L << 21)) {
@@ -899,39 +912,41 @@ static void sweep_one(Engine& E, int k, const Tile& t) {
         dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
         const size_t shm = sizeof(double) * 4 * RING * PL;
         k_sweep_smem<EA, M><<<grd, blk, shm, E.stream>>>(E.P[k], E.F[k], L, E.bc, chunk);
-        return;
+        return false;
     }
     if (D == 3 && E.sweep_minb == 4 && __builtin_popcount(M) > 1)
-        k_sweep_fast<D, EA, M, 4><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
+        k_sweep_fast<D, EA, M, 4><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, ph);
     else
-        k_sweep_fast<D, EA, M><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc);
+        k_sweep_fast<D, EA, M><<<t.grid, t.block, 0, E.stream>>>(E.P[k], E.F[k], L, E.bc, ph);
+    return fused;
 }
 
 template <int D, int EA>
-static void sweep_mask(Engine& E, int k, unsigned m, const Tile& t) {
+static bool sweep_mask(Engine& E, int k, unsigned m, const Tile& t) {
     if (D == 3) {
         switch (m) {
-            case 0x96u: sweep_one<D, EA, 0x96u>(E, k, t); return;
-            case 0x69u: sweep_one<D, EA, 0x69u>(E, k, t); return;
-            case 0x01u: sweep_one<D, EA, 0x01u>(E, k, t); return;
-            case 0x02u: sweep_one<D, EA, 0x02u>(E, k, t); return;
-            case 0x04u: sweep_one<D, EA, 0x04u>(E, k, t); return;
-            case 0x08u: sweep_one<D, EA, 0x08u>(E, k, t); return;
-            case 0x10u: sweep_one<D, EA, 0x10u>(E, k, t); return;
-            case 0x20u: sweep_one<D, EA, 0x20u>(E, k, t); return;
-            case 0x40u: sweep_one<D, EA, 0x40u>(E, k, t); return;
-            case 0x80u: sweep_one<D, EA, 0x80u>(E, k, t); return;
+            case 0x96u: return sweep_one<D, EA, 0x96u>(E, k, t);
+            case 0x69u: return sweep_one<D, EA, 0x69u>(E, k, t);
+            case 0x01u: return sweep_one<D, EA, 0x01u>(E, k, t);
+            case 0x02u: return sweep_one<D, EA, 0x02u>(E, k, t);
+            case 0x04u: return sweep_one<D, EA, 0x04u>(E, k, t);
+            case 0x08u: return sweep_one<D, EA, 0x08u>(E, k, t);
+            case 0x10u: return sweep_one<D, EA, 0x10u>(E, k, t);
+            case 0x20u: return sweep_one<D, EA, 0x20u>(E, k, t);
+            case 0x40u: return sweep_one<D, EA, 0x40u>(E, k, t);
+            case 0x80u: return sweep_one<D, EA, 0x80u>(E, k, t);
         }
     } else {
         switch (m) {
-            case 0x6u: sweep_one<D, EA, 0x6u>(E, k, t); return;
-            case 0x9u: sweep_one<D, EA, 0x9u>(E, k, t); return;
-            case 0x1u: sweep_one<D, EA, 0x1u>(E, k, t); return;
-            case 0x2u: sweep_one<D, EA, 0x2u>(E, k, t); return;
-            case 0x4u: sweep_one<D, EA, 0x4u>(E, k, t); return;
-            case 0x8u: sweep_one<D, EA, 0x8u>(E, k, t); return;
+            case 0x6u: return sweep_one<D, EA, 0x6u>(E, k, t);
+            case 0x9u: return sweep_one<D, EA, 0x9u>(E, k, t);
+            case 0x1u: return sweep_one<D, EA, 0x1u>(E, k, t);
+            case 0x2u: return sweep_one<D, EA, 0x2u>(E, k, t);
+            case 0x4u: return sweep_one<D, EA, 0x4u>(E, k, t);
+            case 0x8u: return sweep_one<D, EA, 0x8u>(E, k, t);
         }
     }
+    return false;
 }
 
 // dispatch the runtime edge axis onto the compile-time one
@@ -969,8 +984,10 @@ static void launch_pad_all(Engine& E, double* P, const Lvl& L, const BcSpec& bc,
 }
 
 // ---- slab exchanges (no-ops on a single rank) ----
+// pushed: the sweep kernel already stored the planes into the peers (fused
+// push) -- only the counters are published
 template <int D>
-static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt) {
+static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt, bool pushed = false) {
     if (!E.sharded(k)) return;
     const Lvl& L = E.L[k];
     const int r = E.rank, P = E.nranks;
@@ -984,15 +1001,22 @@ static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt) {
     const long n = (long)L.B[1] * (D == 3 ? L.B[2] : 1);
     const dim3 grid(nb(n, TPB), 1 << D);
     if (r + 1 < P && up) {
-        k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r + 1].P[k], L, L, L.B[0], 0, up);
+        if (!pushed) {
+            k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r + 1].P[k], L, L, L.B[0],
+                                                         0, up);
+            ++cnt;
+        }
         k_signal<<<1, 1, 0, E.stream>>>(E.peers[r + 1].flags + r, E.cnt + (r + 1));
-        cnt += 2;
+        ++cnt;
     }
     if (r > 0 && dn) {
-        k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r - 1].P[k], L, L, 1,
-                                                     L.B[0] + 1, dn);
+        if (!pushed) {
+            k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r - 1].P[k], L, L, 1,
+                                                         L.B[0] + 1, dn);
+            ++cnt;
+        }
         k_signal<<<1, 1, 0, E.stream>>>(E.peers[r - 1].flags + r, E.cnt + (r - 1));
-        cnt += 2;
+        ++cnt;
     }
     if (r > 0 && up) {
         k_wait<<<1, 1, 0, E.stream>>>(E.flags + (r - 1), E.cnt + P + (r - 1));
@@ -1124,14 +1148,15 @@ static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false,
     for (int it = 0; it < E.s; ++it)
         for (unsigned m : E.masks) {
             if (skip_last && ++done == total) return;
+            bool pushed = false;
             if (first_corr && it == 0 && m == E.masks[0] && done <= 1) {
                 launch_sweep_corr(E, k, m);
                 first_corr = false;
             } else {
-                EA_DISPATCH(D, E.ea, (sweep_mask<D, EA>(E, k, m, t)));
+                EA_DISPATCH(D, E.ea, (pushed = sweep_mask<D, EA>(E, k, m, t)));
             }
             ++cnt;
-            halo_exchange<D>(E, k, m, cnt);
+            halo_exchange<D>(E, k, m, cnt, pushed);
         }
 }
 
@@ -1719,6 +1744,7 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
     if (const char* v = getenv("FASMG_TILE_Y")) g_tile_y = std::max(1, atoi(v));
     if (const char* v = getenv("FASMG_SWEEP_MINB")) E->sweep_minb = atoi(v);
     if (const char* v = getenv("FASMG_EDGE_FAST")) E->edge_fast = atoi(v);
+    if (const char* v = getenv("FASMG_FUSE_PUSH")) E->fuse_push = atoi(v);
     // sharded levels: a prefix of the hierarchy, never the coarsest
     E->kg = 0;
     if (nranks > 1) {

@@ -122,6 +122,34 @@ __device__ __forceinline__ void write_pads(double* __restrict__ P, const Lvl& L,
     }
 }
 
+// ------------------------------------------------------ fused halo push
+// Slab ranks (multi-GPU): the neighbours' halo planes of this level's array
+// (peer memory over NVLink, or the same device for virtual ranks).  A sweep
+// that writes a point of its first/last local block plane also stores it
+// straight into the neighbour's halo plane -- the exchange of the updated
+// classes is fused into the compute kernel (no separate push launch); the
+// host then only publishes the release/acquire counter.  q0=0 classes of
+// plane B0 feed the upper rank's plane 0, q0=1 classes of plane 1 the lower
+// rank's plane B0+1 (the same routing as k_push_plane).
+struct PeerHalo {
+    double* lo = nullptr;
+    double* hi = nullptr;
+};
+
+template <int D>
+__device__ __forceinline__ void push_halo(const PeerHalo& ph, const Lvl& L, int c, const int* bb,
+                                          double v) {
+    constexpr int BIT0 = 1 << (D - 1);
+    if (ph.hi && !(c & BIT0) && bb[0] == L.B[0]) {
+        ph.hi[at<D>(L, c, 0, bb[1], bb[2])] = v;
+        __threadfence_system();
+    }
+    if (ph.lo && (c & BIT0) && bb[0] == 1) {
+        ph.lo[at<D>(L, c, L.B[0] + 1, bb[1], bb[2])] = v;
+        __threadfence_system();
+    }
+}
+
 // ------------------------------------------------------------- pad fill
 // Initialize every pad/wall slot of a level from its interior (after a
 // pack, a restriction or an edge correction).  Launch: grid.y = face id
@@ -173,7 +201,8 @@ __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
 // independent classes; PKG/smoothers.py:136-153).  Thread per block.
 template <int D, int EA, unsigned MASK>
 __device__ __forceinline__ void sweep_pt(double* __restrict__ P, const double* __restrict__ F,
-                                         const Lvl& L, const BcSpec& bc, const int* bb) {
+                                         const Lvl& L, const BcSpec& bc, const int* bb,
+                                         const PeerHalo& ph = PeerHalo()) {
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
     constexpr int NC = 1 << D;
     // phase 1: issue every load of every class before any arithmetic, so
@@ -220,16 +249,17 @@ __device__ __forceinline__ void sweep_pt(double* __restrict__ P, const double* _
         const long o = o0 + (long)c * L.cls;
         P[o] = nv[c];
         if (bnd) write_pads<D, EA>(P, L, bc, c, bb, o, nv[c]);
+        push_halo<D>(ph, L, c, bb, nv[c]);
     }
 }
 
 template <int D, int EA, unsigned MASK, int MINB = 3>
 __global__ void __launch_bounds__(256, MINB) k_sweep_fast(double* __restrict__ P,
                                                     const double* __restrict__ F, Lvl L,
-                                                    BcSpec bc) {
+                                                    BcSpec bc, PeerHalo ph = PeerHalo()) {
     int bb[3];
     if (!tile_coords<D>(L, bb)) return;
-    sweep_pt<D, EA, MASK>(P, F, L, bc, bb);
+    sweep_pt<D, EA, MASK>(P, F, L, bc, bb, ph);
 }
 
 // Same update, one thread per (block, class): grid.z enumerates (b0, k-th

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                                                    double* __restrict__ P, Lvl L, BcSpec bc,
                                                    int chunk, const double* __restrict__ Pc = nullptr,
                                                    const double* __restrict__ PIc = nullptr,
-                                                   Lvl Lc = Lvl()) {
+                                                   Lvl Lc = Lvl(), PeerHalo ph = PeerHalo()) {
     using namespace tsw;
     constexpr unsigned OPP = MASK ^ 0xFFu;
     extern __shared__ __align__(128) double sm[];
@@ -534,6 +534,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 const long o = pl + (long)c * L.cls;
                 P[o] = nv[c];
                 if (bnd) write_pads<3, EA>(P, L, bc, c, bb, o, nv[c]);
+                push_halo<3>(ph, L, c, bb, nv[c]);
             }
             if (CORR && bnd) {  // ghosts of the (uncorrected in memory) B points
 #pragma unroll
@@ -701,7 +702,7 @@ template <int EA, unsigned MASK>
 __global__ void __launch_bounds__(256) k_sweep_tma2d(const __grid_constant__ CUtensorMap mapH,
                                                      const __grid_constant__ CUtensorMap mapF,
                                                      double* __restrict__ P, Lvl L, BcSpec bc,
-                                                     int steps) {
+                                                     int steps, PeerHalo ph = PeerHalo()) {
     using namespace tsw2;
     constexpr unsigned OPP = MASK ^ 0xFu;
     extern __shared__ __align__(128) double sm[];
@@ -767,6 +768,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma2d(const __grid_constant__ CUt
                 const long o = pl + (long)c * L.cls;
                 P[o] = nv[c];
                 if (bnd) write_pads<2, EA>(P, L, bc, c, bb, o, nv[c]);
+                push_halo<2>(ph, L, c, bb, nv[c]);
             }
         }
         __syncthreads();  // slot s is refilled by the next step's prefetch
