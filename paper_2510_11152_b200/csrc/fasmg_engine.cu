@@ -89,11 +89,13 @@ template <int D>
 __device__ __forceinline__ int qbit(int c, int axis) { return (c >> (D - 1 - axis)) & 1; }
 
 // is (class c, block bb) an interior point? (edge axis: class-0 block B is
-// the high wall)
+// the high wall; axis 0 compares the GLOBAL block index on a slab)
 template <int D>
 __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
     if (L.ea < 0) return true;
-    return !(qbit<D>(c, L.ea) == 0 && bb[L.ea] == L.B[L.ea]);
+    const int g = L.ea == 0 ? bb[0] + L.off0 : bb[L.ea];
+    const int B = L.ea == 0 ? L.G0 : L.B[L.ea];
+    return !(qbit<D>(c, L.ea) == 0 && g == B);
 }
 
 #include "fasmg_stencil.cuh"
@@ -102,7 +104,9 @@ __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
 #include "fasmg_fused.cuh"
 
 // ------------------------------------------------- edge-centered transfers
-// Reader of raw stored values at core (grid) index x in the blocked layout.
+// Reader of raw stored values at GLOBAL core (grid) index x in the blocked
+// layout (on an axis-0 slab the block index is shifted by the slab offset;
+// the positions a transfer reads stay within the slab and its halo planes).
 template <int D>
 struct BlkReader {
     const double* P;
@@ -115,6 +119,7 @@ struct BlkReader {
             c |= (x[a] & 1) << (D - 1 - a);
             b[a] = (x[a] + 1) >> 1;
         }
+        b[0] -= L.off0;
         return P[at<D>(L, c, b[0], b[1], b[2])];
     }
 };
@@ -243,6 +248,7 @@ struct CorrReader {
             b[a] = (x[a] + 1) >> 1;
             if (a == L.ea && x[a] == 0) wall = true;
         }
+        b[0] -= L.off0;
         long o = at<D>(L, c, b[0], b[1], b[2]);
         if (wall) return Pc[o];
         return sb(Pc[o], PI[o]);
@@ -331,7 +337,7 @@ __device__ __forceinline__ bool grid_idx(const Lvl& L, int c, const int* b, int*
     bool in = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        x[a] = 2 * b[a] - qbit<D>(c, a);
+        x[a] = 2 * (b[a] + (a == 0 ? L.off0 : 0)) - qbit<D>(c, a);  // global index
         const bool edge = a == L.ea;
         const int hi = edge ? L.n[a] : L.n[a] + 1;
         if (x[a] < 0 || x[a] > hi) return false;
@@ -379,6 +385,14 @@ __global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, 
     }
 }
 
+// coarse rows along axis 0 a fine level's blocks restrict to: all m0 of
+// them, or on a slab those of the local blocks off0+1..off0+B0 (fine block
+// I <-> coarse index I) that are interior
+__host__ __device__ __forceinline__ long restrict_rows(const Lvl& L, long m0) {
+    const long r = (long)L.B[0] < m0 - L.off0 ? (long)L.B[0] : m0 - L.off0;
+    return r > 0 ? r : 0;
+}
+
 // restrict_edge on raw reads (pads of Fn filled by k_pad_all).  Thread per
 // coarse interior point I (natural order, last axis fastest): fine edge-
 // axis columns 2I-1 (class bit 1) and 2I (bit 0) of block I; tangential
@@ -392,6 +406,8 @@ __global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __rest
     long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     long m[3];
     for (int a = 0; a < 3; ++a) m[a] = a < D ? (a == P0 ? Lc.n[a] - 1 : Lc.n[a]) : 1;
+    // axis 0 on a slab: the coarse points of this rank's fine blocks
+    m[0] = restrict_rows(L, m[0]);
     if (t >= m[0] * m[1] * m[2]) return;
     int I[3];
     if (D == 3) {
@@ -405,6 +421,7 @@ __global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __rest
         I[0] = 1 + (int)(t / m[1]);
     }
     const long base = at<D>(L, 0, I[0], I[1], D == 3 ? I[2] : 0);
+    I[0] += L.off0;  // global coarse index from here on
     // fine value: edge offset de (0: 2I-1, 1: 2I), tangential dj/dk (0: 2J-1,
     // 1: 2J, 2: 2J+1)
     auto F = [&](int de, int dj, int dk) {
@@ -442,6 +459,7 @@ __global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __rest
         cc |= (I[a] & 1) << (D - 1 - a);
         cb[a] = (I[a] + 1) >> 1;
     }
+    cb[0] -= Lc.off0;
     Co[at<D>(Lc, cc, cb[0], cb[1], cb[2])] = res;
 }
 
@@ -503,7 +521,8 @@ __global__ void __launch_bounds__(TPB) k_correct_edge_fast(double* __restrict__ 
     int bb[3];
     if (!tile_coords<D>(L, bb)) return;  // 2D/3D thread tile: no 64-bit div/mod
     constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = D == 3 ? (P0 == 2 ? 1 : 2) : 0;
-    const int be = bb[P0], bj = bb[P1], bk = D == 3 ? bb[P2] : 0;
+    const int gb[3] = {bb[0] + L.off0, bb[1], bb[2]};  // global block (axis-0 slab)
+    const int be = gb[P0], bj = gb[P1], bk = D == 3 ? gb[P2] : 0;
     // the block's fine values first (independent of the coarse loads below)
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
     double pv[1 << D];
@@ -728,6 +747,7 @@ struct Engine {
     struct Peer {                       // device pointers of every rank, valid in this process
         double* P[32];
         double* F[32];
+        double* R[32];                  // edge residual arrays (null for cell fields)
         long long* flags;
         double* allpart;
     };
@@ -986,9 +1006,14 @@ static void launch_pad_all(Engine& E, double* P, const Lvl& L, const BcSpec& bc,
 // ---- slab exchanges (no-ops on a single rank) ----
 // pushed: the sweep kernel already stored the planes into the peers (fused
 // push) -- only the counters are published
+// arr: 0 the level's P arrays, 1 its R arrays (edge residual, whose
+// restriction reads the halo plane when axis 0 is tangential)
 template <int D>
-static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt, bool pushed = false) {
+static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt, bool pushed = false,
+                          int arr = 0) {
     if (!E.sharded(k)) return;
+    double* mine = arr ? E.R[k] : E.P[k];
+    auto theirs = [&](int q) { return arr ? E.peers[q].R[k] : E.peers[q].P[k]; };
     const Lvl& L = E.L[k];
     const int r = E.rank, P = E.nranks;
     const unsigned bit0 = 1u << (D - 1);
@@ -1002,8 +1027,7 @@ static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt, bool pushe
     const dim3 grid(nb(n, TPB), 1 << D);
     if (r + 1 < P && up) {
         if (!pushed) {
-            k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r + 1].P[k], L, L, L.B[0],
-                                                         0, up);
+            k_push_plane<D><<<grid, TPB, 0, E.stream>>>(mine, theirs(r + 1), L, L, L.B[0], 0, up);
             ++cnt;
         }
         k_signal<<<1, 1, 0, E.stream>>>(E.peers[r + 1].flags + r, E.cnt + (r + 1));
@@ -1011,8 +1035,8 @@ static void halo_exchange(Engine& E, int k, unsigned mask, long& cnt, bool pushe
     }
     if (r > 0 && dn) {
         if (!pushed) {
-            k_push_plane<D><<<grid, TPB, 0, E.stream>>>(E.P[k], E.peers[r - 1].P[k], L, L, 1,
-                                                         L.B[0] + 1, dn);
+            k_push_plane<D><<<grid, TPB, 0, E.stream>>>(mine, theirs(r - 1), L, L, 1, L.B[0] + 1,
+                                                         dn);
             ++cnt;
         }
         k_signal<<<1, 1, 0, E.stream>>>(E.peers[r - 1].flags + r, E.cnt + (r - 1));
@@ -1258,7 +1282,12 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
             EA_DISPATCH(D, E.ea, (k_residual_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
                                      E.P[k], E.F[k], E.R[k], L)));
             long mc = 1;
-            for (int a = 0; a < D; ++a) mc *= (a == E.ea ? Lc.n[a] - 1 : Lc.n[a]);
+            for (int a = 0; a < D; ++a) {
+                const long ma = a == E.ea ? Lc.n[a] - 1 : Lc.n[a];
+                mc *= a == 0 ? restrict_rows(L, ma) : ma;
+            }
+            // tangential axis 0: the restriction of r reads the upper halo plane
+            if (E.ea != 0) halo_exchange<D>(E, k, ALL, cnt, false, 1);
             if (E.edge_fast) {
                 launch_pad_all<D>(E, E.P[k], L, E.bc, cnt);
                 launch_pad_all<D>(E, E.R[k], L, E.bch, cnt);
@@ -1274,13 +1303,16 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
                 k_restrict_edge<D><<<nb(mc, TPB), TPB, 0, E.stream>>>(E.R[k], L, E.bch,
                                                                       E.F[k + 1], Lc);
             }
-            long tot = Lc.cls * (1 << D);
-            k_copy_blk<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], tot);
-            cnt += 4;
+            cnt += 3;
             launch_pad_fill<D>(E, k + 1, cnt);
         }
         if (E.sharded(k + 1)) halo_exchange<D>(E, k + 1, ALL, cnt);
         else if (E.sharded(k)) gather_level<D>(E, k + 1, cnt);
+        if (E.ea >= 0) {  // pinit = R p, copied after the exchange: halo planes too
+            const long tot = Lc.cls * (1 << D);
+            k_copy_blk<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], tot);
+            ++cnt;
+        }
         EA_DISPATCH(D, E.ea, (k_coarse_src_fast<D, EA><<<tc.grid, tc.block, 0, E.stream>>>(
                                  E.P[k + 1], E.F[k + 1], Lc)));
         ++cnt;
@@ -1712,9 +1744,8 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         fasmg_set_error(FASMG_EINVAL, "bad nranks/rank");
         return nullptr;
     }
-    if (nranks > 1 && (ea >= 0 || kinds[0] == BC_PERIODIC)) {
-        fasmg_set_error(FASMG_EINVAL,
-                        "slab decomposition supports cell-centered fields without periodic x");
+    if (nranks > 1 && kinds[0] == BC_PERIODIC) {
+        fasmg_set_error(FASMG_EINVAL, "slab decomposition needs a non-periodic axis 0");
         return nullptr;
     }
     Engine* E = new Engine();
@@ -1745,6 +1776,7 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
     if (const char* v = getenv("FASMG_SWEEP_MINB")) E->sweep_minb = atoi(v);
     if (const char* v = getenv("FASMG_EDGE_FAST")) E->edge_fast = atoi(v);
     if (const char* v = getenv("FASMG_FUSE_PUSH")) E->fuse_push = atoi(v);
+    if (nranks > 1) E->edge_fast = 1;  // the slab-aware edge transfers
     // sharded levels: a prefix of the hierarchy, never the coarsest
     E->kg = 0;
     if (nranks > 1) {
@@ -1828,13 +1860,14 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
 
 // Number of device pointers fasmg_engine_export writes: P[0..nl), F[0..nl),
 // flags, allpart.
-int fasmg_engine_export_count(void* h) { return 2 * ((Engine*)h)->nl + 2; }
+int fasmg_engine_export_count(void* h) { return 3 * ((Engine*)h)->nl + 2; }
 
 int fasmg_engine_export(void* h, unsigned long long* out) {
     Engine* E = (Engine*)h;
     int t = 0;
     for (int k = 0; k < E->nl; ++k) out[t++] = (unsigned long long)E->P[k];
     for (int k = 0; k < E->nl; ++k) out[t++] = (unsigned long long)E->F[k];
+    for (int k = 0; k < E->nl; ++k) out[t++] = (unsigned long long)E->R[k];
     out[t++] = (unsigned long long)E->flags;
     out[t++] = (unsigned long long)E->allpart;
     return 0;
@@ -1846,18 +1879,19 @@ int fasmg_engine_export(void* h, unsigned long long* out) {
 int fasmg_engine_connect(void* h, const unsigned long long* all, int nranks) {
     Engine* E = (Engine*)h;
     if (nranks != E->nranks) return fasmg_set_error(FASMG_EINVAL, "nranks mismatch");
-    const int per = 2 * E->nl + 2;
+    const int per = 3 * E->nl + 2;
     E->peers.assign(nranks, Engine::Peer());
     for (int r = 0; r < nranks; ++r) {
         const unsigned long long* x = all + (long)r * per;
         Engine::Peer& pr = E->peers[r];
-        for (int k = 0; k < 32; ++k) { pr.P[k] = nullptr; pr.F[k] = nullptr; }
+        for (int k = 0; k < 32; ++k) pr.P[k] = pr.F[k] = pr.R[k] = nullptr;
         for (int k = 0; k < E->nl; ++k) {
             pr.P[k] = (double*)x[k];
             pr.F[k] = (double*)x[E->nl + k];
+            pr.R[k] = (double*)x[2 * E->nl + k];
         }
-        pr.flags = (long long*)x[2 * E->nl];
-        pr.allpart = (double*)x[2 * E->nl + 1];
+        pr.flags = (long long*)x[3 * E->nl];
+        pr.allpart = (double*)x[3 * E->nl + 1];
     }
     return 0;
 }
@@ -1927,7 +1961,10 @@ int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double
     const Lvl& L = E->L[0];
     int e[3];
     for (int a = 0; a < 3; ++a) e[a] = a < E->dim ? (a == E->ea ? L.n[a] + 1 : L.n[a] + 2) : 1;
-    if (E->sharded(0)) e[0] = 2 * L.B[0] + 2;  // rank-local slab (+1 ghost plane each side)
+    if (E->sharded(0)) {  // rank-local slab (+1 ghost plane each side)
+        e[0] = 2 * L.B[0] + 2;
+        if (E->ea == 0 && E->rank == E->nranks - 1) e[0] -= 1;  // edge axis ends at the wall n
+    }
     long tot = (long)e[0] * e[1] * e[2];
     if (E->dim == 3) {
         k_pack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(pcore, ps[0], ps[1], ps[2], E->P[0], L,
@@ -1952,7 +1989,10 @@ int fasmg_engine_store(void* h, double* pcore, const long* ps) {
     const Lvl& L = E->L[0];
     int m[3];
     for (int a = 0; a < 3; ++a) m[a] = a < E->dim ? (a == E->ea ? L.n[a] - 1 : L.n[a]) : 1;
-    if (E->sharded(0)) m[0] = 2 * L.B[0];
+    if (E->sharded(0)) {
+        m[0] = 2 * L.B[0];
+        if (E->ea == 0 && E->rank == E->nranks - 1) m[0] -= 1;  // the last node is the wall
+    }
     long tot = (long)m[0] * m[1] * m[2];
     if (E->dim == 3)
         k_unpack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], ps[2],

@@ -56,7 +56,10 @@ def slab_cells(n0: int, nranks: int, rank: int):
 
 def slab_view(data: torch.Tensor, halo: int, n0: int, nranks: int, rank: int) -> torch.Tensor:
     """The rank's cells along axis 0 plus one ghost plane on each side, as a
-    view of the global C-order data array (core index 0 at data g-1)."""
+    view of the global C-order data array (core index 0 at data g-1).  For
+    a field whose edge axis is axis 0 the same core range holds the rank's
+    nodes (the interface node belongs to the lower rank); the last rank's
+    view ends at the wall node n when the array has no ring beyond it."""
     lo, hi = slab_cells(n0, nranks, rank)
     return data[halo - 1 + lo - 1: halo - 1 + hi + 2]
 
@@ -65,8 +68,6 @@ class _SlabEngine:
     def __init__(self, hierarchy: GridHierarchy, location: Location, bc: BoundaryCondition,
                  plan: SweepPlan, coeffs: OperatorCoeffs, s: int, nranks: int, rank: int,
                  device: torch.device, min_planes: int = 4, stream=None):
-        if location is not Location.CELL:
-            raise NativeError("slab decomposition supports cell-centered fields")
         g = hierarchy.fine
         kinds, vals = bc.codes()
         masks = plan.class_masks()
@@ -79,9 +80,10 @@ class _SlabEngine:
         else:
             self._own_stream = False
         self.stream = stream
+        ea = -1 if location is Location.CELL else location.edge_axis
         with torch.cuda.device(device):
             h = N.lib().fasmg_engine_create_slab(
-                g.dim, N.ints(g.shape), -1, float(g.domain_min[0]), float(g.domain_max[0]),
+                g.dim, N.ints(g.shape), ea, float(g.domain_min[0]), float(g.domain_max[0]),
                 hierarchy.mesh_level, float(coeffs.a), float(coeffs.b), N.ints(kinds),
                 N.doubles(vals), len(masks), (ctypes.c_uint * len(masks))(*masks), int(s),
                 self.stream, int(nranks), int(rank), int(min_planes))
@@ -282,11 +284,15 @@ class DistSlabSolver:
         self._opened = []
 
         def handle_of(ptr):
+            if not ptr:  # arrays a cell-centred engine does not allocate
+                return None
             buf = ctypes.create_string_buffer(64)
             N.check(N.lib().fasmg_ipc_get_handle(ctypes.c_void_p(ptr), buf))
             return buf.raw
 
         def open_handle(hd):
+            if hd is None:
+                return 0
             out = ctypes.c_void_p()
             N.check(N.lib().fasmg_ipc_open_handle(hd, ctypes.byref(out)))
             self._opened.append(out.value)

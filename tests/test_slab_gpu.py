@@ -103,8 +103,9 @@ def test_virtual_slabs_push_modes(P, monkeypatch, fuse):
     assert torch.equal(p1.data, p2.data)
 
 
-@pytest.mark.parametrize("tma_min", ["0", "2097152"])
-def test_two_process_slabs_ipc(tma_min):
+@pytest.mark.parametrize("tma_min,loc", [("0", "cell"), ("2097152", "cell"), ("0", "edge_ew"),
+                                         ("2097152", "edge_ns")])
+def test_two_process_slabs_ipc(tma_min, loc):
     """Two processes (one slab each, sharing the device through CUDA IPC
     peer pointers) run scripts/dist_selftest.py: each rank's slab bitwise
     equal to the single-engine solve."""
@@ -112,10 +113,52 @@ def test_two_process_slabs_ipc(tma_min):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SELFTEST_N="128", FASMG_TMA_MIN=tma_min)
+    env = dict(os.environ, SELFTEST_N="128", FASMG_TMA_MIN=tma_min, SELFTEST_LOC=loc)
+    port = 29600 + int(tma_min != "0") + 2 * ["cell", "edge_ew", "edge_ns"].index(loc)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + int(tma_min != "0")),
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(root, "scripts", "dist_selftest.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert r.stdout.count("field bitwise True, history True") == 2, r.stdout
+
+
+@pytest.mark.parametrize("loc,n,dim,parts,bc,halo,tma_min", [
+    ("edge_ew", 64, 3, 2, "dirichlet", 1, None), ("edge_ew", 64, 3, 4, "lid", 2, None),
+    ("edge_ns", 64, 3, 2, "dirichlet", 1, None), ("edge_tb", 64, 3, 4, "lid", 2, None),
+    ("edge_ew", 128, 3, 4, "neumann_a1", 1, "0"), ("edge_ns", 128, 3, 8, "lid", 2, "0"),
+    ("edge_tb", 128, 3, 2, "dirichlet_val", 1, "0"),
+    ("edge_ew", 256, 2, 4, "dirichlet", 1, None), ("edge_ns", 256, 2, 4, "lid", 2, None),
+])
+def test_virtual_slabs_edge_fields(P, monkeypatch, loc, n, dim, parts, bc, halo, tma_min):
+    """Edge-centred (MAC face-velocity) fields on axis-0 slabs -- the edge
+    axis along the slab axis (edge_ew: the interface node belongs to the
+    lower rank) or tangential to it (the residual's halo plane is exchanged
+    for the tangential restriction): bitwise equal to the single engine."""
+    import cases as C
+    from paper_2510_11152_b200.slab import VirtualSlabSolver
+    if tma_min is not None:
+        monkeypatch.setenv("FASMG_TMA_MIN", tma_min)
+    shape = (n,) * dim
+    spec = "neumann" if bc == "neumann_a1" else bc
+    faces = C.bc_faces(dim, spec)
+    bcond = P.BoundaryCondition(dim, tuple((k, P.FaceRule(*v)) for k, v in faces.items()))
+    L = getattr(P.Location, loc.upper())
+    ml = int(np.log2(n)) - 1
+    p0 = C.rand_field(31, shape, loc, halo)
+    f0 = C.rand_field(32, shape, loc, halo)
+    g = P.unit_grid(shape)
+    coeffs = P.OperatorCoeffs(1.0, 0.05 if bc == "lid" else 0.5)
+    plan = P.make_plan("x", dim)
+    params = P.FasParams(1e-30, 3, 2, ml)
+    p1 = P.Field(g, L, halo, p0.copy())
+    f1 = P.Field(g, L, halo, f0.copy())
+    rep1 = P.FasSolver(P.make_hierarchy(g, ml), L, bcond, plan, coeffs).solve(p1, f1, params)
+    p2 = P.Field(g, L, halo, p0.copy())
+    f2 = P.Field(g, L, halo, f0.copy())
+    vs = VirtualSlabSolver(P.make_hierarchy(g, ml), L, bcond, plan, coeffs, parts)
+    rep2 = vs.solve(p2, f2, params)
+    assert all(e.kg >= 1 for e in vs.engines(params.s, p2.device))  # levels really split
+    np.testing.assert_allclose(rep2.residual_history, rep1.residual_history, rtol=1e-12)
+    assert torch.equal(p1.interior, p2.interior)
+    assert torch.equal(p1.data, p2.data)
