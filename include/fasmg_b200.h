@@ -121,6 +121,16 @@ int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, con
 int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, double* scratch,
                    double* sums, double* out, void* stream);
 long fasmg_view_sum_chunks(int dim, const int* ext);
+/* Slab form of the same reduction (SURVEY.md section 8e item v): per-chunk
+ * sums of an axis-0 slab `ext` of an interior view whose WHOLE extent is
+ * `gext`, with numpy's chunk length for gext (fasmg_view_chunk_len); the
+ * slab must hold whole chunks.  Ranks all-gather the sums in rank order and
+ * total them in chunk order (fasmg_chunk_total, or the same sequential
+ * adds on the host). */
+int fasmg_view_chunk_sums(const double* v, const long* vs, int dim, const int* ext,
+                          const int* gext, double* scratch, double* sums, void* stream);
+long fasmg_view_chunk_len(int dim, const int* gext);
+int fasmg_chunk_total(const double* sums, long nch, double* out, void* stream);
 /* v -= total[0] / count over an interior view */
 int fasmg_sub_mean(double* v, const long* vs, int dim, const int* ext, const double* total,
                    double count, void* stream);

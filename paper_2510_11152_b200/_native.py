@@ -49,6 +49,8 @@ _SIGS = {
     "fasmg_fill_ghosts": "piIiiIDS",
     "fasmg_view_sum": "psiIpppS",
     "fasmg_sub_mean": "psiIpdS",
+    "fasmg_view_chunk_sums": "psiIIppS",
+    "fasmg_chunk_total": "plpS",
     "fasmg_engine_load": "vpsps",
     "fasmg_engine_store": "vps",
     "fasmg_engine_run": "viiDi",
@@ -100,6 +102,8 @@ def lib():
         L.fasmg_version.restype = ctypes.c_int
         L.fasmg_view_sum_chunks.argtypes = [ctypes.c_int, _c_int_p]
         L.fasmg_view_sum_chunks.restype = ctypes.c_long
+        L.fasmg_view_chunk_len.argtypes = [ctypes.c_int, _c_int_p]
+        L.fasmg_view_chunk_len.restype = ctypes.c_long
         L.fasmg_engine_create.argtypes = [
             ctypes.c_int, _c_int_p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
             ctypes.c_int, ctypes.c_double, ctypes.c_double, _c_int_p, _c_double_p,

@@ -954,18 +954,30 @@ int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, con
     return fasmg_check_launch();
 }
 
-// np.sum of an interior view in numpy's buffered-reduce order; result into
-// out[0] (device).  scratch: >= n doubles; sums: >= ceil(n/B) doubles.
-int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, double* scratch,
-                   double* sums, double* out, void* stream) {
-    long n = 1;
-    for (int a = 0; a < dim; ++a) n *= ext[a];
+// numpy's buffered-reduce chunk length for a C-order view of extent ext
+static long np_chunk(int dim, const int* ext) {
     long B = 8192;
     for (int k = 0; k < dim; ++k) {
         long P = 1;
         for (int a = k; a < dim; ++a) P *= ext[a];
         if (P <= 8192) { B = (8192 / P) * P; break; }
     }
+    return B;
+}
+
+// Per-chunk sums of an interior view, the chunk length B taken from the
+// extent gext of the WHOLE array the view belongs to (an axis-0 slab of it:
+// the slab must hold whole chunks, so its sums are a contiguous run of the
+// global chunk list).  scratch: >= n doubles; sums: >= ceil(n/B) doubles.
+int fasmg_view_chunk_sums(const double* v, const long* vs, int dim, const int* ext,
+                          const int* gext, double* scratch, double* sums, void* stream) {
+    long n = 1;
+    for (int a = 0; a < dim; ++a) n *= ext[a];
+    const long B = np_chunk(dim, gext);
+    bool same = true;
+    for (int a = 0; a < dim; ++a) same = same && ext[a] == gext[a];
+    if (!same && n % B)
+        return fasmg_set_error(FASMG_EINVAL, "slab does not hold whole summation chunks");
     long nch = (n + B - 1) / B;
     S3 s = mk(vs);
     if (dim == 2) s.s[2] = 0;
@@ -989,21 +1001,35 @@ int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, dou
                                                           dim == 3 ? ext[2] : 1, n, B, scratch,
                                                           sums, nch);
     }
+    return fasmg_check_launch();
+}
+
+// Sequential total of nch chunk sums in chunk order into out[0] (device).
+int fasmg_chunk_total(const double* sums, long nch, double* out, void* stream) {
     k_chunk_total<<<1, 32, 0, S(stream)>>>(sums, nch, out);
     return fasmg_check_launch();
+}
+
+// np.sum of an interior view in numpy's buffered-reduce order; result into
+// out[0] (device).  scratch: >= n doubles; sums: >= ceil(n/B) doubles.
+int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, double* scratch,
+                   double* sums, double* out, void* stream) {
+    long n = 1;
+    for (int a = 0; a < dim; ++a) n *= ext[a];
+    const long nch = (n + np_chunk(dim, ext) - 1) / np_chunk(dim, ext);
+    if (int st = fasmg_view_chunk_sums(v, vs, dim, ext, ext, scratch, sums, stream)) return st;
+    return fasmg_chunk_total(sums, nch, out, stream);
 }
 
 long fasmg_view_sum_chunks(int dim, const int* ext) {
     long n = 1;
     for (int a = 0; a < dim; ++a) n *= ext[a];
-    long B = 8192;
-    for (int k = 0; k < dim; ++k) {
-        long P = 1;
-        for (int a = k; a < dim; ++a) P *= ext[a];
-        if (P <= 8192) { B = (8192 / P) * P; break; }
-    }
+    const long B = np_chunk(dim, ext);
     return (n + B - 1) / B;
 }
+
+// chunk length numpy uses for a view of extent gext
+long fasmg_view_chunk_len(int dim, const int* gext) { return np_chunk(dim, gext); }
 
 // v -= total[0] / count over an interior view (PKG/fas.py:145,156)
 int fasmg_sub_mean(double* v, const long* vs, int dim, const int* ext, const double* total,

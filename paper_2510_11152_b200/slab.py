@@ -249,6 +249,53 @@ class VirtualSlabSolver:
         return SolveReport(len(history), history, bool(history and history[-1] <= params.tol))
 
 
+def ordered_total(gathered) -> float:
+    """Sequential sum, in chunk order, of every rank's chunk sums gathered in
+    rank order (axis-0 slabs are contiguous runs of the C-order chunk list):
+    the same adds, in the same order, as numpy's buffered reduction of the
+    whole view (SURVEY.md section 8e item v)."""
+    acc = 0.0
+    for part in gathered:
+        for x in part.tolist():
+            acc += x
+    return acc
+
+
+def slab_chunk_sums(v: torch.Tensor, global_ext) -> torch.Tensor:
+    """Per-chunk sums (numpy's chunk length for the whole view of extent
+    ``global_ext``) of this rank's axis-0 slab ``v`` of an interior view."""
+    dim = v.dim()
+    gext = N.ints(global_ext)
+    B = int(N.lib().fasmg_view_chunk_len(dim, gext))
+    nch = (v.numel() + B - 1) // B
+    scratch = torch.empty(max(v.numel(), 1), dtype=torch.float64, device=v.device)
+    sums = torch.empty(max(nch, 1), dtype=torch.float64, device=v.device)
+    N.call("fasmg_view_chunk_sums", N.ptr(v), N.strides(v), dim, N.ints(v.shape), gext,
+           N.ptr(scratch), N.ptr(sums), N.torch_stream())
+    return sums[:nch]
+
+
+def dist_subtract_interior_mean(v: torch.Tensor, global_ext, group=None) -> float:
+    """``interior -= np.mean(interior)`` over a field split into axis-0
+    slabs (PKG/fas.py:145,156 on a decomposed field): ``v`` is this rank's
+    slab of the interior view of extent ``global_ext``.  The chunk sums are
+    all-gathered in rank order (NCCL on device tensors; gloo through host
+    copies) and totalled in chunk order, so the result is bitwise the
+    single-array ``subtract_interior_mean``.  Returns the mean."""
+    import torch.distributed as dist
+    sums = slab_chunk_sums(v, global_ext)
+    world = dist.get_world_size(group)
+    src = sums if dist.get_backend(group) == "nccl" else sums.cpu()
+    out = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(out, src, group=group)
+    total = ordered_total([o.cpu() for o in out])
+    count = float(math.prod(global_ext))
+    tot = torch.tensor([total], dtype=torch.float64, device=v.device)
+    N.call("fasmg_sub_mean", N.ptr(v), N.strides(v), v.dim(), N.ints(v.shape), N.ptr(tot),
+           count, N.torch_stream())
+    return total / count
+
+
 def exchange_ipc(engine_exports, handle_of, open_handle, all_gather_object, rank, world):
     """Turn this rank's exported device pointers into every rank's pointers
     valid in this process: export CUDA-IPC handles, all-gather them,
@@ -278,7 +325,7 @@ class DistSlabSolver:
         self.dist, self.group = dist, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.hierarchy, self.bc, self.coeffs = hierarchy, bc, coeffs
+        self.hierarchy, self.bc, self.coeffs, self.location = hierarchy, bc, coeffs, location
         self.engine = _SlabEngine(hierarchy, location, bc, plan, coeffs, s, self.world,
                                   self.rank, device, min_planes)
         self._opened = []
@@ -330,6 +377,41 @@ class DistSlabSolver:
 
     def store(self, pv: torch.Tensor, halo_p: int = 1):
         self.engine.store(pv, halo_p)
+
+    def _singular(self) -> bool:
+        return self.coeffs.a == 0.0 and all(r.kind != "dirichlet" for _, r in self.bc.faces)
+
+    def _interior(self, v: torch.Tensor, halo: int) -> torch.Tensor:
+        """This rank's rows of the interior view, from its slab view."""
+        g = self.hierarchy.fine
+        ea = self.location.edge_axis
+        m0 = 2 * self.engine.planes
+        if ea == 0 and self.rank == self.world - 1:
+            m0 -= 1  # the wall node n
+        sl = [slice(1, 1 + m0)]
+        for a in range(1, g.dim):
+            m = g.shape[a] - 1 if a == ea else g.shape[a]
+            sl.append(slice(halo, halo + m))  # core 1 sits at data index halo
+        return v[tuple(sl)]
+
+    def solve(self, pv: torch.Tensor, fv: torch.Tensor, params: FasParams, halo_p: int = 1,
+              halo_f: int = 1) -> SolveReport:
+        """FasSolver.solve on this rank's slab views (PKG/fas.py:137-162): for a
+        singular problem f is shifted to zero mean in place first and p after,
+        with the distributed ordered mean; the slab's ghost values are left
+        to the caller (``ghosts_fresh`` False in the reference)."""
+        g = self.hierarchy.fine
+        gext = tuple(g.shape[a] - 1 if a == self.location.edge_axis else g.shape[a]
+                     for a in range(g.dim))
+        singular = self._singular()
+        if singular:
+            dist_subtract_interior_mean(self._interior(fv, halo_f), gext, self.group)
+        self.load(pv, fv, halo_p, halo_f)
+        rep = self.solve_loaded(params)
+        self.store(pv, halo_p)
+        if singular:
+            dist_subtract_interior_mean(self._interior(pv, halo_p), gext, self.group)
+        return rep
 
     def close(self):
         for ptr in self._opened:

@@ -103,9 +103,11 @@ def test_virtual_slabs_push_modes(P, monkeypatch, fuse):
     assert torch.equal(p1.data, p2.data)
 
 
-@pytest.mark.parametrize("tma_min,loc", [("0", "cell"), ("2097152", "cell"), ("0", "edge_ew"),
-                                         ("2097152", "edge_ns")])
-def test_two_process_slabs_ipc(tma_min, loc):
+@pytest.mark.parametrize("tma_min,loc,bc", [("0", "cell", "dirichlet"), ("2097152", "cell", "dirichlet"),
+                                            ("0", "edge_ew", "dirichlet"),
+                                            ("2097152", "edge_ns", "dirichlet"),
+                                            ("2097152", "cell", "neumann")])
+def test_two_process_slabs_ipc(tma_min, loc, bc):
     """Two processes (one slab each, sharing the device through CUDA IPC
     peer pointers) run scripts/dist_selftest.py: each rank's slab bitwise
     equal to the single-engine solve."""
@@ -113,8 +115,10 @@ def test_two_process_slabs_ipc(tma_min, loc):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SELFTEST_N="128", FASMG_TMA_MIN=tma_min, SELFTEST_LOC=loc)
-    port = 29600 + int(tma_min != "0") + 2 * ["cell", "edge_ew", "edge_ns"].index(loc)
+    env = dict(os.environ, SELFTEST_N="128", FASMG_TMA_MIN=tma_min, SELFTEST_LOC=loc,
+               SELFTEST_BC=bc)
+    port = 29600 + int(tma_min != "0") + 2 * ["cell", "edge_ew", "edge_ns"].index(loc) + \
+        10 * (bc == "neumann")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(root, "scripts", "dist_selftest.py")]
