@@ -149,6 +149,14 @@ int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
 int fasmg_laplacian(double* out, const long* os, const double* pcore, const long* ps, int dim,
                     const int* m, double inv_h2, void* stream);
 
+/* momentum source of one velocity component in one pass (NS driver,
+ * Table 3/5 step 1): out = ((u - s0*conv) - s0*(p[x+e_axis]-p[x])*inv_h)
+ * [+ s1*Lap(u)] for order 2; out/conv interior views, u/p core views */
+int fasmg_ns_rhs(int order, double* out, const long* os, const double* ucore, const long* us,
+                 const double* conv, const long* cs, const double* pcore, const long* ps,
+                 int dim, int axis, const int* m, double s0, double s1, double inv_h,
+                 double inv_h2, void* stream);
+
 /* ---- (b2) solver engine: FasSolver (PKG/fas.py:63-162) ------------------ */
 /* FasSolver.__init__ (PKG/fas.py:71-89): n[dim] finest cells, mesh_level
  * coarsenings, operator a*p - b*Lap(p) (PKG/stencil.py:21-38), smoothing
@@ -160,6 +168,18 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
                           const double* vals, int nmasks, const unsigned* masks, int s,
                           void* stream);
 void fasmg_engine_destroy(void* engine);
+/* Engines that never run concurrently (the momentum and pressure solves of
+ * one projection step) can share their level arrays: create them in one
+ * arena.  An engine that finds another engine was the last user of the
+ * arrays clears them on load (the state of a fresh engine), so results are
+ * unchanged.  The arena lives until it and every engine in it are
+ * released. */
+void* fasmg_arena_create(void);
+void fasmg_arena_release(void* arena);
+void* fasmg_engine_create_in(int dim, const int* n, int ea, double dmin, double dmax,
+                             int mesh_level, double a, double b, const int* kinds,
+                             const double* vals, int nmasks, const unsigned* masks, int s,
+                             void* stream, void* arena);
 /* copy p and f (core views, strides) into the engine (enqueued on the
  * engine stream) */
 int fasmg_engine_load(void* engine, const double* pcore, const long* ps, const double* fcore,

@@ -51,6 +51,7 @@ _SIGS = {
     "fasmg_sub_mean": "psiIpdS",
     "fasmg_view_chunk_sums": "psiIIppS",
     "fasmg_chunk_total": "plpS",
+    "fasmg_ns_rhs": "ipspspspsiiIddddS",
     "fasmg_engine_load": "vpsps",
     "fasmg_engine_store": "vps",
     "fasmg_engine_run": "viiDi",
@@ -112,6 +113,12 @@ def lib():
         L.fasmg_engine_create_slab.argtypes = L.fasmg_engine_create.argtypes + [
             ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.fasmg_engine_create_slab.restype = _vp
+        L.fasmg_engine_create_in.argtypes = L.fasmg_engine_create.argtypes + [_vp]
+        L.fasmg_engine_create_in.restype = _vp
+        L.fasmg_arena_create.argtypes = []
+        L.fasmg_arena_create.restype = _vp
+        L.fasmg_arena_release.argtypes = [_vp]
+        L.fasmg_arena_release.restype = None
         L.fasmg_engine_export_count.argtypes = [_vp]
         L.fasmg_engine_export_count.restype = ctypes.c_int
         L.fasmg_engine_export.argtypes = [_vp, ctypes.POINTER(ctypes.c_ulonglong)]

@@ -43,6 +43,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "fasmg_common.cuh"
@@ -713,6 +714,18 @@ __global__ void k_sum_partials(const double* __restrict__ allpart, int n, double
 // ===========================================================================
 // Host engine
 // ===========================================================================
+// Level arrays shared by engines that never run concurrently (the four
+// solves of a projection step run one after another on one stream): the
+// i-th array a level requests is the same buffer in every engine bound to
+// the arena.  An engine that finds another engine was the last user clears
+// all its arrays on load, i.e. starts from the state of a fresh engine.
+struct Arena {
+    int refs = 1;
+    const void* last = nullptr;
+    std::map<std::pair<int, int>, std::pair<size_t, double*>> buf;
+};
+static thread_local Arena* t_arena = nullptr;  // set by fasmg_engine_create_in
+
 struct Engine {
     int dim, ea, nl, s;
     Lvl L[32];
@@ -752,6 +765,8 @@ struct Engine {
         double* allpart;
     };
     std::vector<Peer> peers;            // size nranks once connected
+    Arena* arena = nullptr;             // shared level arrays (nullptr: private)
+    std::vector<void*> owned;           // level arrays this engine frees
     bool sharded(int k) const { return nranks > 1 && k < kg; }
     // ---- temporally blocked smoothing (fasmg_wave.cuh) ----
     int wave_T = 0;                     // FASMG_WAVE_T: half-sweeps per launch (0: off)
@@ -785,6 +800,24 @@ struct Tile {
 };
 
 // tau / outer norm of level k on the TMA march (cell-centred, unsharded)
+// level array number idx of level k: the arena's buffer, or a private one
+static int lvl_alloc(Engine& E, int k, int idx, size_t bytes, double** out) {
+    if (E.arena) {
+        auto& slot = E.arena->buf[{k, idx}];
+        if (!slot.second) {
+            if (int st = fasmg_check(cudaMalloc(&slot.second, bytes))) return st;
+            slot.first = bytes;
+        }
+        if (slot.first >= bytes) {
+            *out = slot.second;
+            return 0;
+        }
+    }
+    if (int st = fasmg_check(cudaMalloc(out, bytes))) return st;
+    E.owned.push_back(*out);
+    return 0;
+}
+
 static bool resid_tma_level(const Engine& E, int k) {
     return E.resid_tma && E.dim == 3 && E.ea < 0 && E.tma_ok[k] && !E.sharded(k);
 }
@@ -1755,6 +1788,10 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
     E->s = s;
     E->stream = (cudaStream_t)stream;
     E->nranks = nranks;
+    if (t_arena && nranks == 1) {  // slab engines export their arrays: never shared
+        E->arena = t_arena;
+        ++t_arena->refs;
+    }
     E->rank = rank;
     for (int t = 0; t < 3; ++t)
         for (int sd = 0; sd < 2; ++sd) {
@@ -1806,19 +1843,19 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         }
         E->L[k] = L;
         size_t bytes = sizeof(double) * (size_t)E->L[k].cls * (1u << dim);
-        if (fasmg_check(cudaMalloc(&E->P[k], bytes)) || fasmg_check(cudaMalloc(&E->F[k], bytes))) {
+        if (lvl_alloc(*E, k, 0, bytes, &E->P[k]) || lvl_alloc(*E, k, 1, bytes, &E->F[k])) {
             delete E;
             return nullptr;
         }
         cudaMemsetAsync(E->P[k], 0, bytes, E->stream);
         cudaMemsetAsync(E->F[k], 0, bytes, E->stream);
         if (ea < 0 && dim == 3 && nranks == 1 && k >= 1) {  // pinit for the fused correction
-            if (fasmg_check(cudaMalloc(&E->PI[k], bytes))) { delete E; return nullptr; }
+            if (lvl_alloc(*E, k, 2, bytes, &E->PI[k])) { delete E; return nullptr; }
             cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
         }
         if (ea >= 0) {
-            if (fasmg_check(cudaMalloc(&E->R[k], bytes))) { delete E; return nullptr; }
-            if (k >= 1 && fasmg_check(cudaMalloc(&E->PI[k], bytes))) { delete E; return nullptr; }
+            if (lvl_alloc(*E, k, 2, bytes, &E->R[k])) { delete E; return nullptr; }
+            if (k >= 1 && lvl_alloc(*E, k, 3, bytes, &E->PI[k])) { delete E; return nullptr; }
             cudaMemsetAsync(E->R[k], 0, bytes, E->stream);
             if (k >= 1) cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
         }
@@ -1856,6 +1893,29 @@ void* fasmg_engine_create(int dim, const int* n, int ea, double dmin, double dma
                           void* stream) {
     return fasmg_engine_create_slab(dim, n, ea, dmin, dmax, mesh_level, a, b, kinds, vals,
                                     nmasks, masks, s, stream, 1, 0, 0);
+}
+
+void* fasmg_arena_create(void) { return new Arena(); }
+
+void fasmg_arena_release(void* h) {
+    Arena* A = (Arena*)h;
+    if (!A || --A->refs > 0) return;
+    for (auto& kv : A->buf)
+        if (kv.second.second) cudaFree(kv.second.second);
+    delete A;
+}
+
+// fasmg_engine_create with the level arrays taken from `arena` (shared with
+// the other engines created in it; they must not run concurrently)
+void* fasmg_engine_create_in(int dim, const int* n, int ea, double dmin, double dmax,
+                             int mesh_level, double a, double b, const int* kinds,
+                             const double* vals, int nmasks, const unsigned* masks, int s,
+                             void* stream, void* arena) {
+    t_arena = (Arena*)arena;
+    void* h = fasmg_engine_create_slab(dim, n, ea, dmin, dmax, mesh_level, a, b, kinds, vals,
+                                       nmasks, masks, s, stream, 1, 0, 0);
+    t_arena = nullptr;
+    return h;
 }
 
 // Number of device pointers fasmg_engine_export writes: P[0..nl), F[0..nl),
@@ -1937,11 +1997,10 @@ void fasmg_engine_destroy(void* h) {
     if (E->exec_vn) cudaGraphExecDestroy(E->exec_vn);
     if (E->graph_v) cudaGraphDestroy(E->graph_v);
     if (E->graph_vn) cudaGraphDestroy(E->graph_vn);
-    for (int k = 0; k < E->nl; ++k) {
-        cudaFree(E->P[k]);
-        cudaFree(E->F[k]);
-        if (E->R[k]) cudaFree(E->R[k]);
-        if (E->PI[k]) cudaFree(E->PI[k]);
+    for (void* ptr : E->owned) cudaFree(ptr);
+    if (E->arena) {
+        if (E->arena->last == E) E->arena->last = nullptr;
+        fasmg_arena_release(E->arena);
     }
     cudaFree(E->part);
     cudaFree(E->dsum);
@@ -1958,6 +2017,14 @@ void fasmg_engine_destroy(void* h) {
 int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double* fcore,
                       const long* fs) {
     Engine* E = (Engine*)h;
+    if (E->arena && E->arena->last != E) {  // another engine used the arrays: start fresh
+        for (int k = 0; k < E->nl; ++k) {
+            const size_t bytes = sizeof(double) * (size_t)E->L[k].cls * (1u << E->dim);
+            for (double* q : {E->P[k], E->F[k], E->R[k], E->PI[k]})
+                if (q) cudaMemsetAsync(q, 0, bytes, E->stream);
+        }
+        E->arena->last = E;
+    }
     const Lvl& L = E->L[0];
     int e[3];
     for (int a = 0; a < 3; ++a) e[a] = a < E->dim ? (a == E->ea ? L.n[a] + 1 : L.n[a] + 2) : 1;

@@ -689,6 +689,52 @@ __global__ void k_ns_elem(int op, double* out, S3 os, V4 in, double s0, double s
     out[I3(os.s, x[0], x[1], x[2])] = r;
 }
 
+// Momentum source of one velocity component in ONE pass (the order-1 /
+// order-2 RHS of Table 3/5 step 1; order 0: the projection correction
+// u~ - dt*gp of step 4): gp = (p[x+e_axis] - p[x]) * inv_h
+// (k_grad), lap = (nsum - 2d*u) * inv_h2 (k_lap), then NS_RHS1 / NS_RHS2 --
+// the same operations in the same order as those three launches, without
+// the two interior-sized temporaries (16 B/DOF of traffic and, at 1024^3,
+// 17 GB of memory).  x: 1-based core index of the component's interior.
+__global__ void k_ns_rhs(int order, double* out, S3 os, const double* u, S3 us,
+                         const double* conv, S3 cs, const double* p, S3 ps, int dim, int axis,
+                         int m0, int m1, int m2, double s0, double s1, double inv_h,
+                         double inv_h2) {
+    long n = (long)m0 * m1 * (dim == 3 ? m2 : 1);
+    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int x[3];
+    if (dim == 3) {
+        x[2] = 1 + (int)(t % m2);
+        long r = t / m2;
+        x[1] = 1 + (int)(r % m1);
+        x[0] = 1 + (int)(r / m1);
+    } else {
+        x[1] = 1 + (int)(t % m1);
+        x[0] = 1 + (int)(t / m1);
+        x[2] = 0;
+    }
+    const int z = dim == 3 ? 1 : 0;
+    const long pl = I3(ps.s, x[0], x[1], x[2]);
+    const double gp = ml(sb(p[pl + ps.s[axis]], p[pl]), inv_h);
+    const long uo = I3(us.s, x[0], x[1], x[2]);
+    const double uc = u[uo];
+    double r;
+    if (order == 0) {  // projection correction u = u~ - dt*grad p~ (NS_AXPY)
+        r = sb(uc, ml(s0, gp));
+    } else {
+        const double cv = conv[I3(cs.s, x[0] - 1, x[1] - 1, x[2] - z)];
+        r = sb(sb(uc, ml(s0, cv)), ml(s0, gp));
+    }
+    if (order == 2) {
+        double ns = ad(ad(ad(u[uo + us.s[0]], u[uo - us.s[0]]), u[uo + us.s[1]]), u[uo - us.s[1]]);
+        if (dim == 3) ns = ad(ad(ns, u[uo + us.s[2]]), u[uo - us.s[2]]);
+        const double lap = ml(sb(ns, ml(dim == 3 ? 6.0 : 4.0, uc)), inv_h2);
+        r = ad(r, ml(s1, lap));
+    }
+    out[I3(os.s, x[0] - 1, x[1] - 1, x[2] - z)] = r;
+}
+
 // 5/7-point Laplacian (nsum - 2d*c) * inv_h2 (KER/numpy_backend.py:66-88)
 __global__ void k_lap(double* out, S3 os, const double* p, S3 ps, int dim, int m0, int m1,
                       int m2, double inv_h2) {
@@ -1090,6 +1136,20 @@ int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
 }
 
 // Laplacian of a field at its interior points: p core view, out interior-shaped
+// momentum source (k_ns_rhs): out/conv interior views, u and p core views,
+// m[dim] the component's interior extents
+int fasmg_ns_rhs(int order, double* out, const long* os, const double* ucore, const long* us,
+                 const double* conv, const long* cs, const double* pcore, const long* ps,
+                 int dim, int axis, const int* m, double s0, double s1, double inv_h,
+                 double inv_h2, void* stream) {
+    S3 o = mk(os), uu = mk(us), cc = mk(cs), pp = mk(ps);
+    if (dim == 2) { o.s[2] = 0; uu.s[2] = 0; cc.s[2] = 0; pp.s[2] = 0; }
+    long tot = (long)m[0] * m[1] * (dim == 3 ? m[2] : 1);
+    LAUNCH(tot, (k_ns_rhs<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(
+                     order, out, o, ucore, uu, conv, cc, pcore, pp, dim, axis, m[0], m[1],
+                     dim == 3 ? m[2] : 1, s0, s1, inv_h, inv_h2)));
+}
+
 int fasmg_laplacian(double* out, const long* os, const double* pcore, const long* ps, int dim,
                     const int* m, double inv_h2, void* stream) {
     S3 o = mk(os), pp = mk(ps);

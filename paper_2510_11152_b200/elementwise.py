@@ -46,3 +46,21 @@ def laplacian(field, out: torch.Tensor | None = None) -> torch.Tensor:
                               ctypes.c_double(1.0 / (field.grid.h * field.grid.h)),
                               N.torch_stream()))
     return out
+
+
+def momentum_source(order: int, out: torch.Tensor, u, conv: torch.Tensor, p, axis: int,
+                    s0: float, s1: float = 0.0) -> torch.Tensor:
+    """``out = ((u - s0*conv) - s0*grad_axis(p)) [+ s1*Lap(u)]`` on the
+    interior of velocity component ``u`` (Field, fresh ghosts for order 2)
+    in one native pass -- bitwise the RHS1/RHS2 elem of gradient_axis and
+    laplacian temporaries.  order 0: ``out = u - s0*grad_axis(p)`` (the
+    projection correction, bitwise AXPY; ``conv`` unused)."""
+    g = u.grid
+    N.require_cuda(out)
+    uc, pc = u.core, p.core
+    N.call("fasmg_ns_rhs", int(order), N.ptr(out), N.strides(out), N.ptr(uc), N.strides(uc),
+           N.ptr(conv if conv is not None else out), N.strides(conv if conv is not None else out),
+           N.ptr(pc), N.strides(pc), g.dim, int(axis),
+           N.ints(u.interior_shape), float(s0), float(s1), 1.0 / g.h, 1.0 / (g.h * g.h),
+           N.torch_stream())
+    return out

@@ -67,13 +67,17 @@ class _Engine:
         ea = solver.location.edge_axis
         self.device = device
         self.stream = N.engine_stream(device.index)
-        with torch.cuda.device(device):
-            h = N.lib().fasmg_engine_create(
-                g.dim, N.ints(g.shape), -1 if ea is None else ea,
+        args = (g.dim, N.ints(g.shape), -1 if ea is None else ea,
                 float(g.domain_min[0]), float(g.domain_max[0]),
                 solver.hierarchy.mesh_level, float(solver.coeffs.a), float(solver.coeffs.b),
                 N.ints(kinds), N.doubles(vals), len(masks),
                 (ctypes.c_uint * len(masks))(*masks), int(s), self.stream)
+        self.arena = solver.arena  # keeps the arena alive while the engine lives
+        with torch.cuda.device(device):
+            if solver.arena is None:
+                h = N.lib().fasmg_engine_create(*args)
+            else:
+                h = N.lib().fasmg_engine_create_in(*args, solver.arena.handle)
         if not h:
             raise NativeError("fasmg_engine_create failed: "
                               + N.lib().fasmg_last_error().decode(errors="replace"))
@@ -119,6 +123,24 @@ class _Engine:
         return ms.value
 
 
+class EngineArena:
+    """Level arrays shared by the engines of several solvers that never run
+    concurrently (one stream, one solve at a time) -- e.g. the three
+    momentum solves and the pressure solve of a projection step, which then
+    hold one set of multigrid workspaces instead of four."""
+
+    def __init__(self):
+        self.handle = ctypes.c_void_p(N.lib().fasmg_arena_create())
+
+    def __del__(self):
+        try:
+            if self.handle is not None and N._lib is not None:
+                N.lib().fasmg_arena_release(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 class FasSolver:
     """Reusable solver owning one workspace set per level (PKG/fas.py:63-89).
 
@@ -128,7 +150,9 @@ class FasSolver:
     """
 
     def __init__(self, hierarchy: GridHierarchy, location: Location,
-                 bc: BoundaryCondition, plan: SweepPlan, coeffs: OperatorCoeffs):
+                 bc: BoundaryCondition, plan: SweepPlan, coeffs: OperatorCoeffs,
+                 arena: EngineArena | None = None):
+        self.arena = arena
         self.hierarchy = hierarchy
         self.location = location
         self.bc = bc

@@ -32,13 +32,13 @@ import numpy as np
 import torch
 
 from .boundary import BoundaryCondition, FaceRule, fill_ghosts
-from .elementwise import ADD, AXPY, MIX_AVG, MIX_EXT, NEG, RHS1, RHS2, elem, laplacian
+from .elementwise import ADD, AXPY, MIX_AVG, MIX_EXT, NEG, elem, momentum_source
 from .errors import MissingBinding
-from .fas import FasParams, FasSolver, SolveReport
+from .fas import EngineArena, FasParams, FasSolver, SolveReport
 from .grid import Field, GridLevel, Location, make_hierarchy
 from .schedule import COMPONENTS_3D, SlotSchedule, build_schedule
 from .smoothers import make_plan
-from .stencil import OperatorCoeffs, divergence_edges_to_cc, gradient_axis, integral_divergence
+from .stencil import OperatorCoeffs, divergence_edges_to_cc, integral_divergence
 from .weno import weno3_convect
 
 LOC_OF = {"u": Location.EDGE_EW, "v": Location.EDGE_NS, "w": Location.EDGE_TB}
@@ -89,7 +89,7 @@ class ProjectionStepper:
     device fields.  ``slots`` holds exactly the schedule's resident fields."""
 
     def __init__(self, grid: GridLevel, params: NSParams, bcs: dict | None = None,
-                 device=None, forcing=None):
+                 device=None, forcing=None, share_workspaces: bool = True):
         """``forcing(component, t)``: optional body force (interior array of
         the component's edge grid) added to the momentum source as
         ``f += dt*F(t)``, with t = t^{n+1} (order 1, backward Euler) or
@@ -111,10 +111,14 @@ class ProjectionStepper:
         hier = make_hierarchy(grid, ml)
         plan = make_plan("x", self.dim, "ff")
         b_mom = params.dt / params.re if params.order == 1 else params.dt / (2.0 * params.re)
-        self.solvers = {c: FasSolver(hier, LOC_OF[c], self.bcs[c], plan, OperatorCoeffs(1.0, b_mom))
+        # the four solves run one after another: one set of multigrid
+        # workspaces (an engine arena) serves them all
+        self.arena = EngineArena() if share_workspaces else None
+        self.solvers = {c: FasSolver(hier, LOC_OF[c], self.bcs[c], plan, OperatorCoeffs(1.0, b_mom),
+                                     arena=self.arena)
                         for c in self.comps}
         self.solvers["p"] = FasSolver(hier, Location.CELL, self.bcs["p"], plan,
-                                      OperatorCoeffs(0.0, params.dt))
+                                      OperatorCoeffs(0.0, params.dt), arena=self.arena)
         dev = device
         # resident slots (the schedule's accounting): velocity fields carry
         # halo 2 for the WENO stencil, pressure halo 1
@@ -187,22 +191,19 @@ class ProjectionStepper:
             if order == 1:
                 fill_ghosts(un, self.bcs[o])
                 vel.append(un)
-            elif f"{o}_tld" in read:
-                vel.append(self._mix_field(("avg", o), o, MIX_AVG, un, read[f"{o}_tld"]))
+            elif f"{o}_tld" in read:  # one mixture buffer per component
+                vel.append(self._mix_field(o, o, MIX_AVG, un, read[f"{o}_tld"]))
             else:
-                vel.append(self._mix_field(("ext", o), o, MIX_EXT, un, read[f"{o}_nm1"]))
+                vel.append(self._mix_field(o, o, MIX_EXT, un, read[f"{o}_nm1"]))
         target = AXIS_OF[c]
         conv = weno3_convect(tuple(vel), target, out=self._f[c])  # reuse f as conv buffer
-        gp = gradient_axis(read["p_n"], target)
         un = read[f"{c}_n"]
         f = self._f[c]
-        if order == 1:
-            elem(RHS1, f.interior, [un.interior, conv.interior, gp], s0=dt)
-        else:
+        # f = ((u^n - dt*conv) - dt*(grad p^n)_c) [+ dt/(2Re)*Lap(u^n)], one pass
+        if order == 2:
             fill_ghosts(un, self.bcs[c])
-            lap = laplacian(un)
-            elem(RHS2, f.interior, [un.interior, conv.interior, gp, lap], s0=dt,
-                 s1=dt / (2.0 * self.params.re))
+        momentum_source(order, f.interior, un, conv.interior, read["p_n"], target, dt,
+                        dt / (2.0 * self.params.re) if order == 2 else 0.0)
         if self.forcing is not None:
             if order == 1:
                 F = self._force(c, self.t + dt)
@@ -272,8 +273,9 @@ class ProjectionStepper:
                 c = st.comp
                 q, slot = st.writes[0]
                 dst = self.slots[slot]
-                gp = gradient_axis(read["p_tld"], AXIS_OF[c])
-                elem(AXPY, dst.interior, [read[f"{c}_tld"].interior, gp], s0=dt)
+                # u^{n+1} = u~ - dt*(grad p~)_c, one pass
+                momentum_source(0, dst.interior, read[f"{c}_tld"], None, read["p_tld"],
+                                AXIS_OF[c], dt)
                 fill_ghosts(dst, self.bcs[c])
                 self._bind(q, slot)
             elif st.formula == "p_update":
