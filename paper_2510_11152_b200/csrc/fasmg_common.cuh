@@ -14,6 +14,27 @@
 
 namespace fasmg {
 
+// Thread -> point of an e0 x e1 (x e2) box without 64-bit integer division:
+// the innermost axis on blockIdx.x * blockDim.x + threadIdx.x, the outer
+// ones on blockIdx.y (and blockIdx.z).  Launch with box_grid.
+__device__ __forceinline__ bool box_coords(int dim, int e0, int e1, int e2, int* x) {
+    if (dim == 3) {
+        x[2] = blockIdx.x * blockDim.x + threadIdx.x;
+        x[1] = blockIdx.y;
+        x[0] = blockIdx.z;
+        return x[2] < e2 && x[1] < e1 && x[0] < e0;
+    }
+    x[1] = blockIdx.x * blockDim.x + threadIdx.x;
+    x[0] = blockIdx.y;
+    x[2] = 0;
+    return x[1] < e1 && x[0] < e0;
+}
+static inline dim3 box_grid(int dim, int e0, int e1, int e2, int tpb) {
+    if (dim == 3) return dim3((unsigned)((e2 + tpb - 1) / tpb), (unsigned)e1, (unsigned)e0);
+    return dim3((unsigned)((e1 + tpb - 1) / tpb), (unsigned)e0, 1u);
+}
+
+
 // ---------------------------------------------------------------------------
 // exact fp64 primitives (no contraction)
 // ---------------------------------------------------------------------------

@@ -656,20 +656,8 @@ struct V4 { const double* p[4]; S3 s[4]; };
 
 __global__ void k_ns_elem(int op, double* out, S3 os, V4 in, double s0, double s1, int dim,
                           int e0, int e1, int e2) {
-    long n = (long)e0 * e1 * (dim == 3 ? e2 : 1);
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= n) return;
     int x[3];
-    if (dim == 3) {
-        x[2] = (int)(t % e2);
-        long r = t / e2;
-        x[1] = (int)(r % e1);
-        x[0] = (int)(r / e1);
-    } else {
-        x[1] = (int)(t % e1);
-        x[0] = (int)(t / e1);
-        x[2] = 0;
-    }
+    if (!box_coords(dim, e0, e1, e2, x)) return;
     double v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -700,21 +688,12 @@ __global__ void k_ns_rhs(int order, double* out, S3 os, const double* u, S3 us,
                          const double* conv, S3 cs, const double* p, S3 ps, int dim, int axis,
                          int m0, int m1, int m2, double s0, double s1, double inv_h,
                          double inv_h2) {
-    long n = (long)m0 * m1 * (dim == 3 ? m2 : 1);
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= n) return;
     int x[3];
-    if (dim == 3) {
-        x[2] = 1 + (int)(t % m2);
-        long r = t / m2;
-        x[1] = 1 + (int)(r % m1);
-        x[0] = 1 + (int)(r / m1);
-    } else {
-        x[1] = 1 + (int)(t % m1);
-        x[0] = 1 + (int)(t / m1);
-        x[2] = 0;
-    }
+    if (!box_coords(dim, m0, m1, m2, x)) return;
     const int z = dim == 3 ? 1 : 0;
+    x[0] += 1;
+    x[1] += 1;
+    x[2] += z;
     const long pl = I3(ps.s, x[0], x[1], x[2]);
     const double gp = ml(sb(p[pl + ps.s[axis]], p[pl]), inv_h);
     const long uo = I3(us.s, x[0], x[1], x[2]);
@@ -1130,9 +1109,9 @@ int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
     S3 o = mk(os);
     if (dim == 2) o.s[2] = 0;
     long tot = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
-    LAUNCH(tot, (k_ns_elem<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(op, out, o, v, s0, s1, dim,
-                                                                  ext[0], ext[1],
-                                                                  dim == 3 ? ext[2] : 1)));
+    LAUNCH(tot, (k_ns_elem<<<box_grid(dim, ext[0], ext[1], dim == 3 ? ext[2] : 1, 128), 128, 0,
+                             S(stream)>>>(op, out, o, v, s0, s1, dim, ext[0], ext[1],
+                                          dim == 3 ? ext[2] : 1)));
 }
 
 // Laplacian of a field at its interior points: p core view, out interior-shaped
@@ -1145,7 +1124,8 @@ int fasmg_ns_rhs(int order, double* out, const long* os, const double* ucore, co
     S3 o = mk(os), uu = mk(us), cc = mk(cs), pp = mk(ps);
     if (dim == 2) { o.s[2] = 0; uu.s[2] = 0; cc.s[2] = 0; pp.s[2] = 0; }
     long tot = (long)m[0] * m[1] * (dim == 3 ? m[2] : 1);
-    LAUNCH(tot, (k_ns_rhs<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(
+    LAUNCH(tot, (k_ns_rhs<<<box_grid(dim, m[0], m[1], dim == 3 ? m[2] : 1, 128), 128, 0,
+                            S(stream)>>>(
                      order, out, o, ucore, uu, conv, cc, pcore, pp, dim, axis, m[0], m[1],
                      dim == 3 ? m[2] : 1, s0, s1, inv_h, inv_h2)));
 }
