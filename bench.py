@@ -19,10 +19,13 @@ test -- the paper's per-"iteration" time.
   1.09 GB, far larger than the 126 MB L2, so no flush is needed between
   steps.
 * e2e: the same metric through the public API with HOST buffers: each step
-  copies p0 and f from pinned host memory into device Fields, calls
-  ``solve(p, f, coeffs, FasParams(tol, k_max=1, s=2, mesh_level=8), plan,
-  bc)`` (the paper's kMax = 1 timing call: pack, V-cycle, residual norm,
-  unpack, ghost fill) and copies p back to pinned host memory.
+  is one problem of ``FasSolver.solve_host_batch`` -- copy p0 and f from
+  pinned host memory to the device, ``solve(..., FasParams(tol, k_max=1,
+  s=2, mesh_level=8))`` (the paper's kMax = 1 timing call: pack, V-cycle,
+  residual norm, unpack, ghost fill), copy p back to pinned host memory.
+  The batch call overlaps the H2D copy of problem i+1 and the D2H copy of
+  problem i-1 with the solve of problem i; ``e2e.serial`` reports the same
+  calls one problem at a time with nothing overlapped.
 * roofline: the dominant kernel, the finest-level smoothing half-sweep,
   re-timed live with CUDA events on its launch stream; algorithmic bytes =
   12 B per fine DOF per half-sweep (read the opposite-parity half of p and
@@ -371,25 +374,49 @@ def b200_arm(args):
 
     # --- e2e through the public API with host buffers (single GPU: Field +
     #     solve(kMax=1); slabs: per-rank slab copies + DistSlabSolver)
-    e2e_steps = args.e2e_steps or max(3, min(K, 5))
+    e2e_steps = args.e2e_steps or max(3, min(K, 8))
     cur = torch.cuda.current_stream(dev)
+    serial = None
     if world == 1:
         ph = torch.from_numpy(p0).pin_memory()
         fh = torch.empty(shape, dtype=torch.float64).pin_memory()
         fh.copy_(f_dev.data.cpu())
-        out_h = torch.empty(shape, dtype=torch.float64).pin_memory()
+        outs = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(2)]
+        params1 = P.FasParams(1e-9, 1, 2, ml)
         pe = Field(g, Location.CELL, 1, device=dev)
         fe = Field(g, Location.CELL, 1, device=dev)
-        params1 = P.FasParams(1e-9, 1, 2, ml)
 
-        def e2e_step():
+        def serial_step():
             pe.data.copy_(ph, non_blocking=True)
             fe.data.copy_(fh, non_blocking=True)
             solver.solve(pe, fe, params1)
-            out_h.copy_(pe.data, non_blocking=True)
+            outs[0].copy_(pe.data, non_blocking=True)
+
+        # the timed e2e region: e2e_steps independent problems through the
+        # public host-batch API (H2D of problem i+1 and D2H of problem i-1
+        # overlap the solve of problem i)
+        def e2e_run(k):
+            solver.solve_host_batch([ph] * k, [fh] * k, params1,
+                                    out=[outs[i % 2] for i in range(k)])
         h2d = 2 * int(np.prod(shape)) * 8
         d2h = int(np.prod(shape)) * 8 + 8
-        api = "Field(host pinned -> device) + solve(..., FasParams(k_max=1)) + p -> host"
+        api = ("FasSolver.solve_host_batch(host pinned p_i, f_i, FasParams(k_max=1)) over "
+               f"{e2e_steps} problems: H2D p,f -> solve -> D2H p per problem, copies "
+               "pipelined on two streams against the solves")
+        # the same call sequence one problem at a time (no overlap), reported beside it
+        serial_step()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        for _ in range(e2e_steps):
+            serial_step()
+        b.record(cur)
+        torch.cuda.synchronize()
+        serial = {"ms_per_step": a.elapsed_time(b) / e2e_steps,
+                  "api": "Field(host pinned -> device) + solve(kMax=1) + p -> host, one "
+                         "problem at a time"}
+        serial["value"] = dof / (serial["ms_per_step"] * 1e-3) / 1e6
     else:
         ph = pv.cpu().pin_memory()
         fh = fv.cpu().pin_memory()
@@ -405,7 +432,11 @@ def b200_arm(args):
         h2d = 2 * ph.numel() * 8
         d2h = ph.numel() * 8 + 8
         api = "rank slab (host pinned -> device) + DistSlabSolver load/run(1)/store + slab -> host"
-    e2e_step()  # warm-up
+
+        def e2e_run(k):
+            for _ in range(k):
+                e2e_step()
+    e2e_run(2)  # warm-up (allocates the batch API's two staging buffers)
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
@@ -413,8 +444,19 @@ def b200_arm(args):
         dist.barrier()
     t2 = time.time()
     a.record(cur)
-    for _ in range(e2e_steps):
-        e2e_step()
+    if os.environ.get("BENCH_E2E_TRACE"):
+        from torch.profiler import profile, ProfilerActivity
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+            e2e_run(e2e_steps)
+            torch.cuda.synchronize()
+        evs = sorted(prof.events(), key=lambda e: e.time_range.start)
+        t00 = evs[0].time_range.start
+        for e in evs:
+            if "emcpy" in e.name or "ynchronize" in e.name or "alloc" in e.name.lower():
+                print(f"[trace] {e.name[:40]:40s} {(e.time_range.start - t00) / 1e3:9.2f} "
+                      f"{(e.time_range.end - e.time_range.start) / 1e3:9.2f}", file=sys.stderr)
+    else:
+        e2e_run(e2e_steps)
     b.record(cur)
     torch.cuda.synchronize()
     clocks.mark(t2, time.time())
@@ -422,6 +464,8 @@ def b200_arm(args):
     e2e = {"value": dof / (e2e_ms * 1e-3) / 1e6, "unit": "MDOF/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_ms, "steps": e2e_steps, "api": api}
+    if serial is not None:
+        e2e["serial"] = serial
     clocks.stop()
 
     # --- CPU baseline (rank 0, N = 1 only)

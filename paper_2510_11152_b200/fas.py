@@ -161,6 +161,7 @@ class FasSolver:
         self.coeffs = coeffs
         self.use_graph = True
         self._engines: dict = {}
+        self._staging: dict = {}  # solve_host_batch device buffers
 
     def engine(self, s: int, device: torch.device) -> _Engine:
         key = (int(s), device.index)
@@ -218,6 +219,84 @@ class FasSolver:
             p.ghosts_fresh = False
         return SolveReport(iterations=len(history), residual_history=history,
                            converged=bool(history and history[-1] <= params.tol))
+
+    # -- independent problems held in host memory --------------------------
+    def solve_host_batch(self, ps, fs, params: FasParams, out=None, halo: int = 1,
+                         device=None) -> list:
+        """``solve`` over a sequence of independent problems whose arrays
+        live in HOST memory (torch CPU tensors of the full field shape, ghost
+        rings included; pinned memory for asynchronous copies).
+
+        Per problem the result equals ``solve(Field(p), Field(f), params)``
+        bitwise: the solution (with filled ghosts) is written to ``out[i]``
+        (default: ``ps[i]`` in place) and, for a singular problem, the
+        mean-shifted rhs back to ``fs[i]`` as the reference mutates the
+        caller's f (PKG/fas.py:145).
+
+        The copies are pipelined over two device staging buffers: the
+        host->device copy of problem i+1 runs on its own stream while
+        problem i is solved, and the device->host copy of problem i runs on a
+        third stream in the opposite PCIe direction, so a batch costs about
+        max(H2D, solve, D2H) per problem instead of their sum."""
+        n = len(ps)
+        if len(fs) != n or (out is not None and len(out) != n):
+            raise ValueError("ps, fs and out must have the same length")
+        out = list(ps) if out is None else list(out)
+        dev = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        g = self.hierarchy.fine
+        # two staging (p, f) pairs per (device, halo), kept on the solver so
+        # that repeated batches allocate nothing
+        bufs = self._staging.setdefault((dev.index, halo), [])
+        while len(bufs) < min(n, 2):
+            bufs.append((Field(g, self.location, halo, device=dev),
+                         Field(g, self.location, halo, device=dev)))
+        bufs = bufs[:max(1, min(n, 2))]
+        shape = tuple(bufs[0][0].data.shape)
+        for t in (*ps, *fs, *out):
+            if t.device.type != "cpu" or tuple(t.shape) != shape or t.dtype != torch.float64:
+                raise ValueError(f"host arrays must be float64 CPU tensors of shape {shape}")
+        singular = self._singular()
+        comp = torch.cuda.current_stream(dev)
+        h2d = torch.cuda.Stream(dev)
+        d2h = torch.cuda.Stream(dev)
+        drained = [None] * len(bufs)  # event: buffer's last result copied out
+        loaded = [None] * n
+
+        def enqueue_h2d(i):
+            b = i % len(bufs)
+            with torch.cuda.stream(h2d):
+                if drained[b] is not None:
+                    h2d.wait_event(drained[b])
+                bufs[b][0].data.copy_(ps[i], non_blocking=True)
+                bufs[b][1].data.copy_(fs[i], non_blocking=True)
+                loaded[i] = torch.cuda.Event()
+                loaded[i].record(h2d)
+
+        reports = []
+        h2d.wait_stream(comp)  # earlier work on the staging buffers was ordered on comp
+        if n:
+            enqueue_h2d(0)
+        for i in range(n):
+            if i + 1 < n:
+                enqueue_h2d(i + 1)
+            b = i % len(bufs)
+            p, f = bufs[b]
+            p.ghosts_fresh = f.ghosts_fresh = False
+            comp.wait_event(loaded[i])
+            reports.append(self.solve(p, f, params))
+            done = torch.cuda.Event()
+            done.record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                out[i].copy_(p.data, non_blocking=True)
+                if singular:
+                    fs[i].copy_(f.data, non_blocking=True)
+                drained[b] = torch.cuda.Event()
+                drained[b].record(d2h)
+        comp.wait_stream(d2h)
+        comp.wait_stream(h2d)
+        return reports
 
 
 def vcycle(p: Field, f: Field, coeffs: OperatorCoeffs, params: FasParams,
