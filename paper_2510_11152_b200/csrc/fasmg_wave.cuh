@@ -383,24 +383,37 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
     // block (y0-1+r, x0-1+q) at entry r*CX+q; thread tid covers entries tid
     // and tid+256.  corr_fetch only issues the loads (v: Pc, pinit pairs);
     // corr_store subtracts and stores -- a step later, so the latency hides.
-    auto corr_fetch = [&](int pl, double* v) {
+    // The in-plane part of each entry's coarse offset (coarse class bits of
+    // axes 1, 2 and the coarse blocks, coarse_of) is fixed for the launch:
+    // computed once here, so a plane step adds only the axis-0 part.
+    long cofs[2] = {0, 0};
+    bool cok[2] = {false, false};
+    if (CORR) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int e = tid + i * 256;
             const int b1 = y0 - 1 + e / CX, b2 = x0 - 1 + e % CX;
+            cok[i] = e < CB && b1 >= 1 && b1 <= L.B[1] && b2 >= 1 && b2 <= L.B[2];
+            cofs[i] = (long)(((b1 & 1) << 1) | (b2 & 1)) * Lc.cls + (long)((b1 + 1) >> 1) * Lc.s1 +
+                      ((b2 + 1) >> 1) + OFF;
+        }
+    }
+    auto corr_fetch = [&](int pl, double* v) {
+        const int I0 = pl + L.off0;  // global fine block = coarse cell index
+        const long po = (long)((I0 & 1) << 2) * Lc.cls + (long)(((I0 + 1) >> 1) - Lc.off0) * Lc.s0;
+        const bool pok = pl >= 1 && pl <= L.B[0];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
             v[2 * i] = v[2 * i + 1] = 0.0;
-            if (e < CB && pl >= 1 && pl <= L.B[0] && b1 >= 1 && b1 <= L.B[1] && b2 >= 1 &&
-                b2 <= L.B[2]) {
-                int fb[3] = {pl, b1, b2}, cc = 0, cb[3] = {0, 0, 0};
-                coarse_of<3>(L, Lc, fb, cc, cb);
-                const long oc = at<3>(Lc, cc, cb[0], cb[1], cb[2]);
-                v[2 * i] = __ldg(Pc + oc);
-                v[2 * i + 1] = __ldg(PIc + oc);
+            if (pok && cok[i]) {
+                v[2 * i] = __ldg(Pc + po + cofs[i]);
+                v[2 * i + 1] = __ldg(PIc + po + cofs[i]);
             }
         }
     };
+    static_assert((CRING & (CRING - 1)) == 0, "CRING must be a power of two");
     auto corr_store = [&](int pl, const double* v) {
-        double* d = csm + ((pl + CRING) % CRING) * CB;
+        double* d = csm + (pl & (CRING - 1)) * CB;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int e = tid + i * 256;
@@ -466,10 +479,10 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
         double araw[8];
         if (CORR && active) {
             const int cc0 = (ty + 1) * CX + tx + 1;
-            const double* cp = csm + ((b0 + CRING) % CRING) * CB;
+            const double* cp = csm + (b0 & (CRING - 1)) * CB;
             c_own = cp[cc0];
-            cW[0] = csm[((b0 - 1 + CRING) % CRING) * CB + cc0];
-            cE[0] = csm[((b0 + 1) % CRING) * CB + cc0];
+            cW[0] = csm[((b0 - 1) & (CRING - 1)) * CB + cc0];
+            cE[0] = csm[((b0 + 1) & (CRING - 1)) * CB + cc0];
             cW[1] = cp[cc0 - CX];
             cE[1] = cp[cc0 + CX];
             cW[2] = cp[cc0 - 1];
@@ -487,6 +500,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
         mbar_wait(&bar[b0 & 1], ((b0 - b0s) >> 1) & 1);
         if (active) {
             const int ci = (ty + 1) * HX + tx + 2;  // tile centre in a halo box
+            const bool bnd = on_boundary<3>(L, bb);
             double nv[8];
             int j = 0;
 #pragma unroll
@@ -503,18 +517,27 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 double e2 = wz[ci + (q2 ? 0 : 1)], w2 = wz[ci - (q2 ? 1 : 0)];
                 if (CORR) {
                     // inside the block: own correction; across a face: the
-                    // neighbour block's, or (domain face) the own ghost
-                    const double ac = ad(araw[c], c_own);  // corrected value of this point
-                    auto gh = [&](int a, int sd) {
-                        return bc.kind[a][sd] == BC_DIRICHLET ? sb(ml(2.0, bc.val[a][sd]), ac) : ac;
-                    };
-                    const int g0 = gb0(L, bb);
-                    if (q0) { e0 = ad(e0, c_own); w0v = g0 == 1 ? gh(0, 0) : ad(w0v, cW[0]); }
-                    else { w0v = ad(w0v, c_own); e0 = g0 == Bn[0] ? gh(0, 1) : ad(e0, cE[0]); }
-                    if (q1) { e1 = ad(e1, c_own); w1 = bb[1] == 1 ? gh(1, 0) : ad(w1, cW[1]); }
-                    else { w1 = ad(w1, c_own); e1 = bb[1] == Bn[1] ? gh(1, 1) : ad(e1, cE[1]); }
-                    if (q2) { e2 = ad(e2, c_own); w2 = bb[2] == 1 ? gh(2, 0) : ad(w2, cW[2]); }
-                    else { w2 = ad(w2, c_own); e2 = bb[2] == Bn[2] ? gh(2, 1) : ad(e2, cE[2]); }
+                    // neighbour block's ...
+                    if (q0) { e0 = ad(e0, c_own); w0v = ad(w0v, cW[0]); }
+                    else { w0v = ad(w0v, c_own); e0 = ad(e0, cE[0]); }
+                    if (q1) { e1 = ad(e1, c_own); w1 = ad(w1, cW[1]); }
+                    else { w1 = ad(w1, c_own); e1 = ad(e1, cE[1]); }
+                    if (q2) { e2 = ad(e2, c_own); w2 = ad(w2, cW[2]); }
+                    else { w2 = ad(w2, c_own); e2 = ad(e2, cE[2]); }
+                    if (bnd) {  // ... or, across a domain face, the own ghost
+                        const double ac = ad(araw[c], c_own);  // corrected value of this point
+                        auto gh = [&](int a, int sd) {
+                            return bc.kind[a][sd] == BC_DIRICHLET ? sb(ml(2.0, bc.val[a][sd]), ac)
+                                                                  : ac;
+                        };
+                        const int g0 = gb0(L, bb);
+                        if (q0) { if (g0 == 1) w0v = gh(0, 0); }
+                        else if (g0 == Bn[0]) e0 = gh(0, 1);
+                        if (q1) { if (bb[1] == 1) w1 = gh(1, 0); }
+                        else if (bb[1] == Bn[1]) e1 = gh(1, 1);
+                        if (q2) { if (bb[2] == 1) w2 = gh(2, 0); }
+                        else if (bb[2] == Bn[2]) e2 = gh(2, 1);
+                    }
                 }
                 // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:62)
                 double ns = ad(e0, w0v);
@@ -526,7 +549,6 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
-            const bool bnd = on_boundary<3>(L, bb);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (!((MASK >> c) & 1u)) continue;
