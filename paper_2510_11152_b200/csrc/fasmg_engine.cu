@@ -466,45 +466,55 @@ __global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __rest
 
 // Corr = the value CorrReader + ghost chain give at every coarse position a
 // prolongation reads (interior: p_c - pinit; ghosts under the homogenized
-// bc).  Thread per storage element of the coarse level.
+// bc).  Thread per block position (pads included) of the coarse level, all
+// 2^d classes: a 2D/3D thread tile (block axes from the grid, no 64-bit
+// div/mod); interior points are one subtraction, only pad positions take
+// the ghost chain.
 template <int D>
 __global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc,
                                                    const double* __restrict__ PI, Lvl Lc,
                                                    BcSpec bch, double* __restrict__ Corr) {
-    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= Lc.cls * (1L << D)) return;
-    const int c = (int)(t / Lc.cls);
-    long rem = t - (long)c * Lc.cls - OFF;
-    if (rem < 0) return;
     int b[3] = {0, 0, 0};
     if (D == 3) {
-        b[0] = (int)(rem / Lc.s0);
-        rem -= (long)b[0] * Lc.s0;
-        b[1] = (int)(rem / Lc.s1);
-        b[2] = (int)(rem - (long)b[1] * Lc.s1);
-        if (b[0] >= Lc.E[0] || b[2] >= Lc.E[2]) return;
+        b[2] = blockIdx.x * blockDim.x + threadIdx.x;
+        b[1] = blockIdx.y * blockDim.y + threadIdx.y;
+        b[0] = blockIdx.z;
+        if (b[2] >= Lc.E[2] || b[1] >= Lc.E[1]) return;
     } else {
-        b[0] = (int)(rem / Lc.s0);
-        b[1] = (int)(rem - (long)b[0] * Lc.s0);
-        if (b[0] >= Lc.E[0] || b[1] >= Lc.E[1]) return;
+        b[1] = blockIdx.x * blockDim.x + threadIdx.x;
+        b[0] = blockIdx.y * blockDim.y + threadIdx.y;
+        if (b[1] >= Lc.E[1] || b[0] >= Lc.E[0]) return;
     }
-    int x[3] = {0, 0, 0};
-    bool in;
-    if (!grid_idx<D>(Lc, c, b, x, &in)) return;
+    const long o0 = at<D>(Lc, 0, b[0], b[1], b[2]);
     CorrReader<D> rd{Pc, PI, Lc};
-    double v;
-    if (in) {
-        v = rd(x[0], x[1], x[2]);
-    } else {
-        AxisGeo ax[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            ax[q].m = q < D ? Lc.n[q] : 1;
-            ax[q].edge = (q == Lc.ea);
+    for (int c = 0; c < (1 << D); ++c) {
+        int x[3] = {0, 0, 0};
+        bool in;
+        if (!grid_idx<D>(Lc, c, b, x, &in)) continue;
+        const long o = o0 + (long)c * Lc.cls;
+        double v;
+        if (in) {
+            v = sb(Pc[o], PI[o]);
+        } else {
+            AxisGeo ax[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                ax[q].m = q < D ? Lc.n[q] : 1;
+                ax[q].edge = (q == Lc.ea);
+            }
+            v = ghost_value<D>(ax, bch, x[0], x[1], x[2], rd);
         }
-        v = ghost_value<D>(ax, bch, x[0], x[1], x[2], rd);
+        Corr[o] = v;
     }
-    Corr[at<D>(Lc, c, b[0], b[1], b[2])] = v;
+}
+
+// launch geometry of k_corr_edge: every block position 0..E-1 per axis
+template <int D>
+static void corr_edge_grid(const Lvl& Lc, dim3& grd, dim3& blk) {
+    blk = dim3(32, 8, 1);
+    if (D == 3) grd = dim3((Lc.E[2] + 31) / 32, (Lc.E[1] + 7) / 8, Lc.E[0]);
+    else grd = dim3((Lc.E[1] + 31) / 32, (Lc.E[0] + 7) / 8, 1);
 }
 
 // prolong_edge of Corr added to the fine interior (raw reads).  All 2^d
@@ -1367,9 +1377,10 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
             }
         } else {
             if (E.edge_fast) {
-                const long tot = Lc.cls * (1L << D);
-                k_corr_edge<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc,
-                                                                   E.bch, E.R[k + 1]);
+                dim3 cg, cbk;
+                corr_edge_grid<D>(Lc, cg, cbk);
+                k_corr_edge<D><<<cg, cbk, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc, E.bch,
+                                                         E.R[k + 1]);
                 EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<t.grid, t.block, 0,
                                                                    E.stream>>>(E.P[k], L,
                                                                                E.R[k + 1], Lc)));
