@@ -526,7 +526,7 @@ static void corr_edge_grid(const Lvl& Lc, dim3& grd, dim3& blk) {
 // or b+1 (q=0); edge-axis line b (qe=0) or the mean of lines b-1, b (qe=1)
 // -- KER/numpy_backend.py:194-224.
 template <int D, int EA>
-__global__ void __launch_bounds__(TPB) k_correct_edge_fast(double* __restrict__ P, Lvl L,
+__global__ void __launch_bounds__(TPB, 4) k_correct_edge_fast(double* __restrict__ P, Lvl L,
                                                            const double* __restrict__ Corr,
                                                            Lvl Lc) {
     int bb[3];
@@ -759,6 +759,7 @@ struct Engine {
     // same march fed by TMA boxes (default), else 0
     int sweep_variant = 4;
     int march_chunk = 0;    // planes per marching chunk (0: per-level default)
+    int norm_smem = 0;      // dynamic smem of the outer-norm march (FASMG_NORM_SMEM caps CTAs/SM)
     int sweep_minb = 3;     // min resident CTAs of the 3D half-sweep (register cap)
     int edge_fast = 1;      // FASMG_EDGE_FAST: pad-materialised edge transfers (0: ghost chains)
     // ---- axis-0 slab decomposition (multi-GPU / virtual ranks) ----
@@ -1416,7 +1417,7 @@ static void launch_norm(Engine& E, long& cnt, bool fused = false) {
         if (D == 3 && E.resid_tma && E.tma_ok[0] && !E.sharded(0)) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
-            EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA><<<g, dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
+            EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA><<<g, dim3(rsw::TX, rsw::TY, 1), E.norm_smem,
                                                        E.stream>>>(
                                      E.mapT[0], E.P[0], E.F[0], L, E.bc, ch, E.part, nullptr,
                                      nullptr, L, nullptr)));
@@ -1592,12 +1593,18 @@ static int tma_setup(Engine& E) {
     if (const char* v = getenv("FASMG_RESID_TMA")) E.resid_tma = atoi(v);
     if (const char* v = getenv("FASMG_CORR_FUSE")) E.corr_fuse = atoi(v);
     if (const char* v = getenv("FASMG_CORR_CHUNK")) E.corr_chunk = atoi(v);
+    // at most 3 CTAs per SM for the norm march: the EA = 1 instantiation
+    // compiles to 64 registers, so 4 CTAs fit and then stall on the MIO
+    // queue (ncu: mio_throttle, 553 us vs 350 us for the cell one at 3 CTAs);
+    // padding the dynamic smem to 58 KB takes the EDGE_NS V-cycle 8.43 -> 8.09 ms
+    E.norm_smem = std::max((int)rsw::SMEM, 58000);
+    if (const char* v = getenv("FASMG_NORM_SMEM")) E.norm_smem = std::max((int)rsw::SMEM, atoi(v));
     int st = 0;
     EA_DISPATCH(3, E.ea, (st = tma_attr<EA>()));
     if (!st) EA_DISPATCH(3, E.ea, (st = fasmg_check(cudaFuncSetAttribute(
                                         k_resid_tma<0, EA>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)rsw::SMEM))));
+                                        E.norm_smem))));
     if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)rsw::SMEM));
