@@ -14,7 +14,7 @@
 // of the corresponding standalone kernel (sweep_pt, tau_pt, coarse_src_pt,
 // correct_pt in fasmg_stencil.cuh), so the arithmetic and the ghost-pad
 // maintenance are identical and results bitwise equal.  Cell-centered
-// fields only (edge transfers keep their launches).
+// fields only (edge transfers keep their launches: see coarse_setup).
 #pragma once
 
 struct CoarseArgs {

@@ -352,14 +352,14 @@ __device__ __forceinline__ bool grid_idx(const Lvl& L, int c, const int* b, int*
 // the value fill_ghosts gives it under bc (PKG/boundary.py:90-156).  Thread
 // per pad block position of one face (grid.y = face), all classes.
 template <int D>
-__global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, BcSpec bc) {
-    const int face = blockIdx.y, a = face >> 1, side = face & 1;
+__device__ __forceinline__ void pad_all_pt(double* __restrict__ P, const Lvl& L,
+                                           const BcSpec& bc, int face, long t) {
+    const int a = face >> 1, side = face & 1;
     int oth[2], no = 0;
 #pragma unroll
-    for (int t = 0; t < D; ++t)
-        if (t != a) oth[no++] = t;
+    for (int q = 0; q < D; ++q)
+        if (q != a) oth[no++] = q;
     const long n1 = L.E[oth[0]], n2 = D == 3 ? L.E[oth[1]] : 1;
-    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (t >= n1 * n2) return;
     int b[3] = {0, 0, 0};
     b[a] = side ? L.B[a] + 1 : 0;
@@ -386,6 +386,11 @@ __global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, 
     }
 }
 
+template <int D>
+__global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, BcSpec bc) {
+    pad_all_pt<D>(P, L, bc, blockIdx.y, blockIdx.x * (long)blockDim.x + threadIdx.x);
+}
+
 // coarse rows along axis 0 a fine level's blocks restrict to: all m0 of
 // them, or on a slab those of the local blocks off0+1..off0+B0 (fine block
 // I <-> coarse index I) that are interior
@@ -401,10 +406,9 @@ __host__ __device__ __forceinline__ long restrict_rows(const Lvl& L, long m0) {
 // The edge axis is a template parameter so every class/offset is a
 // compile-time constant; the arithmetic is KER/numba_backend.py:304-342.
 template <int D, int EA>
-__global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __restrict__ Fn, Lvl L,
-                                                            double* __restrict__ Co, Lvl Lc) {
+__device__ __forceinline__ void restrict_edge_pt(const double* __restrict__ Fn, const Lvl& L,
+                                                 double* __restrict__ Co, const Lvl& Lc, long t) {
     constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = D == 3 ? (P0 == 2 ? 1 : 2) : 0;
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     long m[3];
     for (int a = 0; a < 3; ++a) m[a] = a < D ? (a == P0 ? Lc.n[a] - 1 : Lc.n[a]) : 1;
     // axis 0 on a slab: the coarse points of this rank's fine blocks
@@ -464,6 +468,12 @@ __global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __rest
     Co[at<D>(Lc, cc, cb[0], cb[1], cb[2])] = res;
 }
 
+template <int D, int EA>
+__global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __restrict__ Fn, Lvl L,
+                                                            double* __restrict__ Co, Lvl Lc) {
+    restrict_edge_pt<D, EA>(Fn, L, Co, Lc, blockIdx.x * (long)blockDim.x + threadIdx.x);
+}
+
 // Corr = the value CorrReader + ghost chain give at every coarse position a
 // prolongation reads (interior: p_c - pinit; ghosts under the homogenized
 // bc).  Thread per block position (pads included) of the coarse level, all
@@ -471,20 +481,10 @@ __global__ void __launch_bounds__(TPB) k_restrict_edge_fast(const double* __rest
 // div/mod); interior points are one subtraction, only pad positions take
 // the ghost chain.
 template <int D>
-__global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc,
-                                                   const double* __restrict__ PI, Lvl Lc,
-                                                   BcSpec bch, double* __restrict__ Corr) {
-    int b[3] = {0, 0, 0};
-    if (D == 3) {
-        b[2] = blockIdx.x * blockDim.x + threadIdx.x;
-        b[1] = blockIdx.y * blockDim.y + threadIdx.y;
-        b[0] = blockIdx.z;
-        if (b[2] >= Lc.E[2] || b[1] >= Lc.E[1]) return;
-    } else {
-        b[1] = blockIdx.x * blockDim.x + threadIdx.x;
-        b[0] = blockIdx.y * blockDim.y + threadIdx.y;
-        if (b[1] >= Lc.E[1] || b[0] >= Lc.E[0]) return;
-    }
+__device__ __forceinline__ void corr_edge_pt(const double* __restrict__ Pc,
+                                             const double* __restrict__ PI, const Lvl& Lc,
+                                             const BcSpec& bch, double* __restrict__ Corr,
+                                             const int* b) {
     const long o0 = at<D>(Lc, 0, b[0], b[1], b[2]);
     CorrReader<D> rd{Pc, PI, Lc};
 #pragma unroll
@@ -509,6 +509,24 @@ __global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc
     }
 }
 
+template <int D>
+__global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc,
+                                                   const double* __restrict__ PI, Lvl Lc,
+                                                   BcSpec bch, double* __restrict__ Corr) {
+    int b[3] = {0, 0, 0};
+    if (D == 3) {
+        b[2] = blockIdx.x * blockDim.x + threadIdx.x;
+        b[1] = blockIdx.y * blockDim.y + threadIdx.y;
+        b[0] = blockIdx.z;
+        if (b[2] >= Lc.E[2] || b[1] >= Lc.E[1]) return;
+    } else {
+        b[1] = blockIdx.x * blockDim.x + threadIdx.x;
+        b[0] = blockIdx.y * blockDim.y + threadIdx.y;
+        if (b[1] >= Lc.E[1] || b[0] >= Lc.E[0]) return;
+    }
+    corr_edge_pt<D>(Pc, PI, Lc, bch, Corr, b);
+}
+
 // launch geometry of k_corr_edge: every block position 0..E-1 per axis
 template <int D>
 static void corr_edge_grid(const Lvl& Lc, dim3& grd, dim3& blk) {
@@ -526,11 +544,9 @@ static void corr_edge_grid(const Lvl& Lc, dim3& grd, dim3& blk) {
 // or b+1 (q=0); edge-axis line b (qe=0) or the mean of lines b-1, b (qe=1)
 // -- KER/numpy_backend.py:194-224.
 template <int D, int EA>
-__global__ void __launch_bounds__(TPB, 4) k_correct_edge_fast(double* __restrict__ P, Lvl L,
-                                                           const double* __restrict__ Corr,
-                                                           Lvl Lc) {
-    int bb[3];
-    if (!tile_coords<D>(L, bb)) return;  // 2D/3D thread tile: no 64-bit div/mod
+__device__ __forceinline__ void correct_edge_pt(double* __restrict__ P, const Lvl& L,
+                                                const double* __restrict__ Corr, const Lvl& Lc,
+                                                const int* bb) {
     constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = D == 3 ? (P0 == 2 ? 1 : 2) : 0;
     const int gb[3] = {bb[0] + L.off0, bb[1], bb[2]};  // global block (axis-0 slab)
     const int be = gb[P0], bj = gb[P1], bk = D == 3 ? gb[P2] : 0;
@@ -568,6 +584,15 @@ __global__ void __launch_bounds__(TPB, 4) k_correct_edge_fast(double* __restrict
         const double v = qe ? ml(ad(line(0), line(1)), 0.5) : line(1);
         P[o0 + (long)c * L.cls] = ad(pv[c], v);
     }
+}
+
+template <int D, int EA>
+__global__ void __launch_bounds__(TPB, 4) k_correct_edge_fast(double* __restrict__ P, Lvl L,
+                                                           const double* __restrict__ Corr,
+                                                           Lvl Lc) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;  // 2D/3D thread tile: no 64-bit div/mod
+    correct_edge_pt<D, EA>(P, L, Corr, Lc, bb);
 }
 
 __global__ void k_final_sum(const double* __restrict__ part, int n, double* out) {
@@ -1323,13 +1348,13 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
                 ++cnt;
             }
         } else {
-            EA_DISPATCH(D, E.ea, (k_residual_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
-                                     E.P[k], E.F[k], E.R[k], L)));
             long mc = 1;
             for (int a = 0; a < D; ++a) {
                 const long ma = a == E.ea ? Lc.n[a] - 1 : Lc.n[a];
                 mc *= a == 0 ? restrict_rows(L, ma) : ma;
             }
+            EA_DISPATCH(D, E.ea, (k_residual_fast<D, EA><<<t.grid, t.block, 0, E.stream>>>(
+                                     E.P[k], E.F[k], E.R[k], L)));
             // tangential axis 0: the restriction of r reads the upper halo plane
             if (E.ea != 0) halo_exchange<D>(E, k, ALL, cnt, false, 1);
             if (E.edge_fast) {
@@ -1621,6 +1646,11 @@ static int coarse_setup(Engine& E) {
     // at once (512 threads x 128 registers each); with virtual ranks sharing
     // a device it can starve behind peers' spin-waits (observed: 8 virtual
     // ranks at 512^3).  Sharded engines keep per-level launches.
+    // Edge fields keep per-level launches: the same scheme with the edge
+    // transfers' phases (residual, pads, two restrictions, pad fill, pinit,
+    // correction, prolongation; all bitwise) measured SLOWER than the
+    // launches it replaced (EDGE_NS 512^3 V-cycle 8.26 -> 8.41 ms: ~16
+    // cluster-barrier phases per level against ~2.5 us per graph launch).
     if (E.ea >= 0 || E.coarse_max <= 0 || E.masks.size() > 16 || E.nranks > 1) return 0;
     int k0 = E.nl;
     while (k0 > 0 && !E.sharded(k0 - 1) && E.L[k0 - 1].nblk <= E.coarse_max) --k0;

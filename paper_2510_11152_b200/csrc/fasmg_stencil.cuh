@@ -155,8 +155,8 @@ __device__ __forceinline__ void push_halo(const PeerHalo& ph, const Lvl& L, int 
 // pack, a restriction or an edge correction).  Launch: grid.y = face id
 // (2*D faces), x over the face's blocks.
 template <int D, int EA>
-__global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
-    const int face = blockIdx.y;
+__device__ __forceinline__ void pad_fill_pt(double* __restrict__ P, const Lvl& L,
+                                            const BcSpec& bc, int face, long t) {
     const int a = face >> 1, side = face & 1;
     // enumerate the other axes' blocks
     int oth[2], no = 0;
@@ -164,7 +164,6 @@ __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
     for (int t = 0; t < D; ++t)
         if (t != a) oth[no++] = t;
     long n1 = L.B[oth[0]], n2 = (D == 3) ? L.B[oth[1]] : 1;
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (t >= n1 * n2) return;
     if (a == 0 && ((side == 0 && L.off0 != 0) || (side == 1 && L.off0 + L.B[0] != L.G0)))
         return;  // internal slab face: the halo comes from the neighbor rank
@@ -194,6 +193,11 @@ __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
         if (is_wall<D, EA>(L, c, bb)) continue;
         write_pads<D, EA>(P, L, bc, c, bb, o, P[o]);
     }
+}
+
+template <int D, int EA>
+__global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
+    pad_fill_pt<D, EA>(P, L, bc, blockIdx.y, blockIdx.x * (long)blockDim.x + threadIdx.x);
 }
 
 // ------------------------------------------------------------- smoothing
@@ -735,11 +739,9 @@ __global__ void __launch_bounds__(256) k_correct_fast(double* __restrict__ P, Lv
 
 // residual into R (edge fields: input of the tangential restriction)
 template <int D, int EA>
-__global__ void __launch_bounds__(256) k_residual_fast(const double* __restrict__ P,
-                                                       const double* __restrict__ F,
-                                                       double* __restrict__ R, Lvl L) {
-    int bb[3];
-    if (!tile_coords<D>(L, bb)) return;
+__device__ __forceinline__ void residual_pt(const double* __restrict__ P,
+                                            const double* __restrict__ F, double* __restrict__ R,
+                                            const Lvl& L, const int* bb) {
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
@@ -747,6 +749,15 @@ __global__ void __launch_bounds__(256) k_residual_fast(const double* __restrict_
         const long o = o0 + (long)c * L.cls;
         R[o] = sb(F[o], op_fast<D>(P, L, c, o));
     }
+}
+
+template <int D, int EA>
+__global__ void __launch_bounds__(256) k_residual_fast(const double* __restrict__ P,
+                                                       const double* __restrict__ F,
+                                                       double* __restrict__ R, Lvl L) {
+    int bb[3];
+    if (!tile_coords<D>(L, bb)) return;
+    residual_pt<D, EA>(P, F, R, L, bb);
 }
 
 // Outer residual sum of squares of a cell-centred level, structured like
