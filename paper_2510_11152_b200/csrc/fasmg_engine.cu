@@ -391,6 +391,16 @@ __global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, 
     pad_all_pt<D>(P, L, bc, blockIdx.y, blockIdx.x * (long)blockDim.x + threadIdx.x);
 }
 
+// the pads of two arrays of one level in one launch (grid.z = 0: P under
+// bc, 1: R under bch) -- the edge tau pass pads p and r together
+template <int D>
+__global__ void __launch_bounds__(TPB) k_pad_all2(double* __restrict__ P, BcSpec bc,
+                                                  double* __restrict__ R, BcSpec bch, Lvl L) {
+    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (blockIdx.z == 0) pad_all_pt<D>(P, L, bc, blockIdx.y, t);
+    else pad_all_pt<D>(R, L, bch, blockIdx.y, t);
+}
+
 // coarse rows along axis 0 a fine level's blocks restrict to: all m0 of
 // them, or on a slab those of the local blocks off0+1..off0+B0 (fine block
 // I <-> coarse index I) that are interior
@@ -1072,6 +1082,21 @@ static void launch_pad_all(Engine& E, double* P, const Lvl& L, const BcSpec& bc,
     ++cnt;
 }
 
+template <int D>
+static void launch_pad_all2(Engine& E, int k, long& cnt) {
+    const Lvl& L = E.L[k];
+    long face = 1;
+    for (int a = 0; a < D; ++a) {
+        long f = 1;
+        for (int t = 0; t < D; ++t)
+            if (t != a) f *= L.E[t];
+        face = std::max(face, f);
+    }
+    k_pad_all2<D><<<dim3(nb(face, TPB), 2 * D, 2), TPB, 0, E.stream>>>(E.P[k], E.bc, E.R[k],
+                                                                        E.bch, L);
+    ++cnt;
+}
+
 // ---- slab exchanges (no-ops on a single rank) ----
 // pushed: the sweep kernel already stored the planes into the peers (fused
 // push) -- only the counters are published
@@ -1358,8 +1383,7 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
             // tangential axis 0: the restriction of r reads the upper halo plane
             if (E.ea != 0) halo_exchange<D>(E, k, ALL, cnt, false, 1);
             if (E.edge_fast) {
-                launch_pad_all<D>(E, E.P[k], L, E.bc, cnt);
-                launch_pad_all<D>(E, E.R[k], L, E.bch, cnt);
+                launch_pad_all2<D>(E, k, cnt);
                 EA_DISPATCH(D, E.ea, (k_restrict_edge_fast<D, EA><<<nb(mc, TPB), TPB, 0,
                                                                     E.stream>>>(E.P[k], L,
                                                                                 E.P[k + 1], Lc)));
