@@ -624,19 +624,18 @@ __global__ void k_final_sum(const double* __restrict__ part, int n, double* out)
 template <int D>
 __global__ void k_pack(const double* __restrict__ src, long s0, long s1, long s2,
                        double* __restrict__ dst, Lvl L, int e0, int e1, int e2) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    long tot = (long)e0 * e1 * (D == 3 ? e2 : 1);
-    if (t >= tot) return;
+    // 2D/3D thread tile (x along the contiguous axis): no 64-bit div/mod
     int x[3];
     if (D == 3) {
-        x[2] = (int)(t % e2);
-        long r = t / e2;
-        x[1] = (int)(r % e1);
-        x[0] = (int)(r / e1);
+        x[2] = blockIdx.x * blockDim.x + threadIdx.x;
+        x[1] = blockIdx.y * blockDim.y + threadIdx.y;
+        x[0] = blockIdx.z;
+        if (x[2] >= e2 || x[1] >= e1) return;
     } else {
-        x[1] = (int)(t % e1);
-        x[0] = (int)(t / e1);
+        x[1] = blockIdx.x * blockDim.x + threadIdx.x;
+        x[0] = blockIdx.y * blockDim.y + threadIdx.y;
         x[2] = 0;
+        if (x[1] >= e1 || x[0] >= e0) return;
     }
     int c = 0, b[3] = {0, 0, 0};
 #pragma unroll
@@ -651,19 +650,17 @@ __global__ void k_pack(const double* __restrict__ src, long s0, long s1, long s2
 template <int D>
 __global__ void k_unpack(const double* __restrict__ src, Lvl L, double* __restrict__ dst,
                          long s0, long s1, long s2, int m0, int m1, int m2) {
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    long tot = (long)m0 * m1 * (D == 3 ? m2 : 1);
-    if (t >= tot) return;
     int x[3];
     if (D == 3) {
-        x[2] = 1 + (int)(t % m2);
-        long r = t / m2;
-        x[1] = 1 + (int)(r % m1);
-        x[0] = 1 + (int)(r / m1);
+        x[2] = 1 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+        x[1] = 1 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+        x[0] = 1 + (int)blockIdx.z;
+        if (x[2] > m2 || x[1] > m1) return;
     } else {
-        x[1] = 1 + (int)(t % m1);
-        x[0] = 1 + (int)(t / m1);
+        x[1] = 1 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+        x[0] = 1 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
         x[2] = 0;
+        if (x[1] > m1 || x[0] > m0) return;
     }
     int c = 0, b[3] = {0, 0, 0};
 #pragma unroll
@@ -672,6 +669,13 @@ __global__ void k_unpack(const double* __restrict__ src, Lvl L, double* __restri
         b[a] = (x[a] + 1) >> 1;
     }
     dst[x[0] * s0 + x[1] * s1 + (long)x[2] * s2] = src[at<D>(L, c, b[0], b[1], b[2])];
+}
+
+// launch geometry of k_pack / k_unpack over an (n0, n1[, n2]) box
+static inline void pack_grid(int dim, int n0, int n1, int n2, dim3& grd, dim3& blk) {
+    blk = dim3(128, 2, 1);
+    if (dim == 3) grd = dim3((n2 + 127) / 128, (n1 + 1) / 2, n0);
+    else grd = dim3((n1 + 127) / 128, (n0 + 1) / 2, 1);
 }
 
 static inline int nb(long n, int t) { return (int)((n + t - 1) / t); }
@@ -2104,17 +2108,16 @@ int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double
         e[0] = 2 * L.B[0] + 2;
         if (E->ea == 0 && E->rank == E->nranks - 1) e[0] -= 1;  // edge axis ends at the wall n
     }
-    long tot = (long)e[0] * e[1] * e[2];
+    dim3 pg, pb;
+    pack_grid(E->dim, e[0], e[1], e[2], pg, pb);
     if (E->dim == 3) {
-        k_pack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(pcore, ps[0], ps[1], ps[2], E->P[0], L,
-                                                        e[0], e[1], e[2]);
-        k_pack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(fcore, fs[0], fs[1], fs[2], E->F[0], L,
-                                                        e[0], e[1], e[2]);
+        k_pack<3><<<pg, pb, 0, E->stream>>>(pcore, ps[0], ps[1], ps[2], E->P[0], L, e[0], e[1],
+                                            e[2]);
+        k_pack<3><<<pg, pb, 0, E->stream>>>(fcore, fs[0], fs[1], fs[2], E->F[0], L, e[0], e[1],
+                                            e[2]);
     } else {
-        k_pack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(pcore, ps[0], ps[1], 0, E->P[0], L, e[0],
-                                                        e[1], 1);
-        k_pack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(fcore, fs[0], fs[1], 0, E->F[0], L, e[0],
-                                                        e[1], 1);
+        k_pack<2><<<pg, pb, 0, E->stream>>>(pcore, ps[0], ps[1], 0, E->P[0], L, e[0], e[1], 1);
+        k_pack<2><<<pg, pb, 0, E->stream>>>(fcore, fs[0], fs[1], 0, E->F[0], L, e[0], e[1], 1);
     }
     long cnt = 0;
     if (E->dim == 3) launch_pad_fill<3>(*E, 0, cnt);
@@ -2132,13 +2135,13 @@ int fasmg_engine_store(void* h, double* pcore, const long* ps) {
         m[0] = 2 * L.B[0];
         if (E->ea == 0 && E->rank == E->nranks - 1) m[0] -= 1;  // the last node is the wall
     }
-    long tot = (long)m[0] * m[1] * m[2];
+    dim3 pg, pb;
+    pack_grid(E->dim, m[0], m[1], m[2], pg, pb);
     if (E->dim == 3)
-        k_unpack<3><<<nb(tot, TPB), TPB, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], ps[2],
-                                                          m[0], m[1], m[2]);
+        k_unpack<3><<<pg, pb, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], ps[2], m[0], m[1],
+                                              m[2]);
     else
-        k_unpack<2><<<nb(tot, TPB), TPB, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], 0,
-                                                          m[0], m[1], 1);
+        k_unpack<2><<<pg, pb, 0, E->stream>>>(E->P[0], L, pcore, ps[0], ps[1], 0, m[0], m[1], 1);
     return fasmg_check_launch();
 }
 
