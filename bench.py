@@ -374,7 +374,7 @@ def b200_arm(args):
 
     # --- e2e through the public API with host buffers (single GPU: Field +
     #     solve(kMax=1); slabs: per-rank slab copies + DistSlabSolver)
-    e2e_steps = args.e2e_steps or max(3, min(K, 8))
+    e2e_steps = args.e2e_steps or max(3, K)
     cur = torch.cuda.current_stream(dev)
     serial = None
     if world == 1:
