@@ -85,13 +85,16 @@ def dist_env():
 
 def config_dict(n, dim, parallelism):
     ml = int(np.log2(n)) - 1
+    fb = (n + 2) ** dim * 8  # bytes of one field
     return {
         "workload": f"heat{dim}d_{n}: backward-Euler step p - dt*Lap(p) = f, dt=1 (a=b=1), "
                     f"cell-centered {n}^{dim}, Dirichlet 0, FAS V-cycle, X-MCGS ff, s=2, "
                     f"meshLevel={ml}, f=L_h(manufactured), p0=U[0,1)",
         "grid": [n] * dim, "mesh_level": ml, "smoother": "X-MCGS ff", "s": 2,
         "step": "one FAS V-cycle + outer residual norm (PKG/fas.py:147-154)",
-        "l2_flush": "not needed: each field is %.2f GB >> 126 MB L2" % ((n + 2) ** dim * 8 / 1e9),
+        "l2_flush": ("not needed: each field is %.2f GB >> 126 MB L2" % (fb / 1e9) if fb > 4 * 126e6
+                     else "none: each field is %.3f GB, not >> 126 MB L2 (functional size, not a "
+                          "bench configuration)" % (fb / 1e9)),
         "parallelism": parallelism,
     }
 
