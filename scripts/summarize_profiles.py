@@ -34,7 +34,11 @@ for k in sorted(L):
     tot[key][0] += 1
     tot[key][1] += t
     tot[key][2] += by
-    if key.startswith("k_sweep_tma") and t > 0:
+    # plain half-sweeps only: the corrected one (template flag true / 1) is a
+    # different kernel with its own coarse reads
+    full = d["name"]
+    corr = ", 1>(" in full or ", true>(" in full or "(bool)1>" in full
+    if key.startswith("k_sweep_tma") and t > 0 and not corr:
         fine_sweeps.append((t, by))
 alltime = sum(v[1] for v in tot.values())
 out.append(f"# {tag}: ncu launch list of one eager V-cycle + norm, 3D {n}^3 heat "
@@ -50,7 +54,7 @@ top = [x for x in fine_sweeps if x[0] >= 0.5 * fine_sweeps[0][0]]
 avg_t = sum(x[0] for x in top) / len(top)
 avg_b = sum(x[1] for x in top) / len(top)
 alg = 12.0 * n ** dim
-out.append(f"finest half-sweeps: {len(top)} launches, mean {avg_t/1e3:.1f} us, dram {avg_b/1e9:.3f} GB "
+out.append(f"finest plain half-sweeps: {len(top)} launches, mean {avg_t/1e3:.1f} us, dram {avg_b/1e9:.3f} GB "
            f"per launch (algorithmic {alg/1e9:.3f} GB, ratio {avg_b/alg:.3f}), "
            f"share of fasmg time {100*sum(x[0] for x in top)/alltime:.1f}%")
 json.dump({"tag": tag, "n": n, "dim": dim, "dram_bytes_per_launch": avg_b,
