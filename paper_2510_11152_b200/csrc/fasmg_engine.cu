@@ -624,58 +624,81 @@ __global__ void k_final_sum(const double* __restrict__ part, int n, double* out)
 template <int D>
 __global__ void k_pack(const double* __restrict__ src, long s0, long s1, long s2,
                        double* __restrict__ dst, Lvl L, int e0, int e1, int e2) {
-    // 2D/3D thread tile (x along the contiguous axis): no 64-bit div/mod
-    int x[3];
+    // 2D/3D thread tile, no 64-bit div/mod.  A thread moves the pair
+    // (2j, 2j+1) of the contiguous axis: class bit 0 of block j and class
+    // bit 1 of block j+1, so a warp reads 64 consecutive doubles and writes
+    // 32 consecutive doubles into each of two class arrays.
+    constexpr int LA = D - 1;  // contiguous axis
+    int x[3] = {0, 0, 0};
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (D == 3) {
-        x[2] = blockIdx.x * blockDim.x + threadIdx.x;
         x[1] = blockIdx.y * blockDim.y + threadIdx.y;
         x[0] = blockIdx.z;
-        if (x[2] >= e2 || x[1] >= e1) return;
+        if (2 * j >= e2 || x[1] >= e1) return;
     } else {
-        x[1] = blockIdx.x * blockDim.x + threadIdx.x;
         x[0] = blockIdx.y * blockDim.y + threadIdx.y;
-        x[2] = 0;
-        if (x[1] >= e1 || x[0] >= e0) return;
+        if (2 * j >= e1 || x[0] >= e0) return;
     }
+    const int eL = D == 3 ? e2 : e1;
+    const long sL = D == 3 ? s2 : s1;
+    const long so = (long)x[0] * s0 + (D == 3 ? (long)x[1] * s1 : 0) + (long)(2 * j) * sL;
+    const bool two = 2 * j + 1 < eL;
+    const double v0 = src[so];
+    const double v1 = two ? src[so + sL] : 0.0;
     int c = 0, b[3] = {0, 0, 0};
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
+    for (int a = 0; a < LA; ++a) {
         c |= (x[a] & 1) << (D - 1 - a);
         b[a] = (x[a] + 1) >> 1;
     }
-    dst[at<D>(L, c, b[0], b[1], b[2])] = src[x[0] * s0 + x[1] * s1 + (long)x[2] * s2];
+    b[LA] = j;  // x = 2j: class bit 0, block j
+    dst[at<D>(L, c, b[0], b[1], b[2])] = v0;
+    if (two) {  // x = 2j + 1: class bit 1, block j + 1
+        b[LA] = j + 1;
+        dst[at<D>(L, c | 1, b[0], b[1], b[2])] = v1;
+    }
 }
 
-// interior only (core indices 1..M)
+// interior only (core indices 1..M).  A thread moves the pair (2j-1, 2j) of
+// the contiguous axis: classes bit 1 and bit 0 of block j.
 template <int D>
 __global__ void k_unpack(const double* __restrict__ src, Lvl L, double* __restrict__ dst,
                          long s0, long s1, long s2, int m0, int m1, int m2) {
-    int x[3];
+    constexpr int LA = D - 1;
+    int x[3] = {0, 0, 0};
+    const int j = 1 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
     if (D == 3) {
-        x[2] = 1 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
         x[1] = 1 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
         x[0] = 1 + (int)blockIdx.z;
-        if (x[2] > m2 || x[1] > m1) return;
+        if (2 * j - 1 > m2 || x[1] > m1) return;
     } else {
-        x[1] = 1 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
         x[0] = 1 + (int)(blockIdx.y * blockDim.y + threadIdx.y);
-        x[2] = 0;
-        if (x[1] > m1 || x[0] > m0) return;
+        if (2 * j - 1 > m1 || x[0] > m0) return;
     }
+    const int mL = D == 3 ? m2 : m1;
+    const long sL = D == 3 ? s2 : s1;
     int c = 0, b[3] = {0, 0, 0};
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
+    for (int a = 0; a < LA; ++a) {
         c |= (x[a] & 1) << (D - 1 - a);
         b[a] = (x[a] + 1) >> 1;
     }
-    dst[x[0] * s0 + x[1] * s1 + (long)x[2] * s2] = src[at<D>(L, c, b[0], b[1], b[2])];
+    b[LA] = j;
+    const long o = at<D>(L, c, b[0], b[1], b[2]);
+    const bool two = 2 * j <= mL;
+    const double v1 = src[o + L.cls];  // x = 2j - 1: class bit 1
+    const double v0 = two ? src[o] : 0.0;  // x = 2j: class bit 0
+    const long so = (long)x[0] * s0 + (D == 3 ? (long)x[1] * s1 : 0) + (long)(2 * j - 1) * sL;
+    dst[so] = v1;
+    if (two) dst[so + sL] = v0;
 }
 
-// launch geometry of k_pack / k_unpack over an (n0, n1[, n2]) box
+// launch geometry of k_pack / k_unpack over an (n0, n1[, n2]) box: x over
+// PAIRS of the contiguous axis
 static inline void pack_grid(int dim, int n0, int n1, int n2, dim3& grd, dim3& blk) {
     blk = dim3(128, 2, 1);
-    if (dim == 3) grd = dim3((n2 + 127) / 128, (n1 + 1) / 2, n0);
-    else grd = dim3((n1 + 127) / 128, (n0 + 1) / 2, 1);
+    if (dim == 3) grd = dim3(((n2 + 1) / 2 + 127) / 128, (n1 + 1) / 2, n0);
+    else grd = dim3(((n1 + 1) / 2 + 127) / 128, (n0 + 1) / 2, 1);
 }
 
 static inline int nb(long n, int t) { return (int)((n + t - 1) / t); }
