@@ -611,28 +611,17 @@ __global__ void k_grad(const double* p, S3 ps, double* out, int dim, int axis, i
 struct Comps { const double* c[3]; S3 s[3]; };
 __global__ void k_div(Comps C, double* out, S3 os, int dim, int n0, int n1, int n2,
                       double inv_h) {
-    long n = (long)n0 * n1 * (dim == 3 ? n2 : 1);
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= n) return;
     int x[3];
-    if (dim == 3) {
-        x[2] = 1 + (int)(t % n2);
-        long r = t / n2;
-        x[1] = 1 + (int)(r % n1);
-        x[0] = 1 + (int)(r / n1);
-    } else {
-        x[1] = 1 + (int)(t % n1);
-        x[0] = 1 + (int)(t / n1);
-        x[2] = 0;
-    }
+    if (!box_coords(dim, n0, n1, n2, x)) return;  // 0-based interior box position
+    const int y0 = x[0] + 1, y1 = x[1] + 1, y2 = dim == 3 ? x[2] + 1 : 0;
     double acc = 0.0;
     for (int a = 0; a < dim; ++a) {
-        long hi = I3(C.s[a].s, x[0], x[1], x[2]);
+        long hi = I3(C.s[a].s, y0, y1, y2);
         long lo = hi - C.s[a].s[a];
         double term = ml(sb(C.c[a][hi], C.c[a][lo]), inv_h);
         acc = a == 0 ? term : ad(acc, term);
     }
-    out[I3(os.s, x[0] - 1, x[1] - 1, x[2] - (dim == 3 ? 1 : 0))] = acc;
+    out[I3(os.s, x[0], x[1], dim == 3 ? x[2] : 0)] = acc;
 }
 
 // ------------------------------------------------ projection-step elementwise
@@ -1092,8 +1081,8 @@ int fasmg_divergence(const double* const* comps, const long* cs, double* out, co
     S3 o = mk(os);
     if (dim == 2) o.s[2] = 0;
     long tot = (long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
-    LAUNCH(tot, (k_div<<<nblk(tot, TPB), TPB, 0, S(stream)>>>(C, out, o, dim, n[0], n[1],
-                                                              dim == 3 ? n[2] : 1, inv_h)));
+    LAUNCH(tot, (k_div<<<box_grid(dim, n[0], n[1], dim == 3 ? n[2] : 1, 128), 128, 0,
+                         S(stream)>>>(C, out, o, dim, n[0], n[1], dim == 3 ? n[2] : 1, inv_h)));
 }
 
 // generic interior elementwise op (NsOp); views: out + up to 4 inputs
