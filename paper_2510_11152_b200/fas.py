@@ -256,6 +256,16 @@ class FasSolver:
         for t in (*ps, *fs, *out):
             if t.device.type != "cpu" or tuple(t.shape) != shape or t.dtype != torch.float64:
                 raise ValueError(f"host arrays must be float64 CPU tensors of shape {shape}")
+        # a result copied out while another problem's input is read from the
+        # same host memory would race (the copies overlap by design)
+        ins = {}
+        for j, t in enumerate((*ps, *fs)):
+            ins.setdefault(t.data_ptr(), set()).add(j % n)
+        written = list(out) + (list(fs) if self._singular() else [])  # singular: f is shifted
+        for i, t in enumerate(written):
+            if ins.get(t.data_ptr(), {i % n}) - {i % n}:
+                raise ValueError(f"a written host array of problem {i % n} shares memory with "
+                                 "the input of another problem")
         singular = self._singular()
         comp = torch.cuda.current_stream(dev)
         h2d = torch.cuda.Stream(dev)

@@ -93,3 +93,15 @@ def test_batch_rejects_bad_lengths():
                     P.make_plan("x", 2), P.OperatorCoeffs(1.0, 1.0))
     with pytest.raises(ValueError):
         S.solve_host_batch([torch.zeros(10, 10)], [], P.FasParams(1e-9, 1, 2, 2))
+
+
+@pytest.mark.gpu
+def test_batch_rejects_output_aliasing_another_input(P):
+    g = P.unit_grid((8, 8, 8))
+    S = P.FasSolver(P.make_hierarchy(g, 2), P.Location.CELL, P.BoundaryCondition.dirichlet(3),
+                    P.make_plan("x", 3), P.OperatorCoeffs(1.0, 1.0))
+    ps, fs = _problems((8, 8, 8), 2, 1)
+    with pytest.raises(ValueError):
+        S.solve_host_batch(ps, fs, P.FasParams(1e-9, 1, 2, 2), out=[ps[1], ps[0]])
+    with pytest.raises(ValueError):  # in place with one tensor for both problems
+        S.solve_host_batch([ps[0], ps[0]], fs, P.FasParams(1e-9, 1, 2, 2))
