@@ -353,22 +353,17 @@ __device__ __forceinline__ bool grid_idx(const Lvl& L, int c, const int* b, int*
 // per pad block position of one face (grid.y = face), all classes.
 template <int D>
 __device__ __forceinline__ void pad_all_pt(double* __restrict__ P, const Lvl& L,
-                                           const BcSpec& bc, int face, long t) {
+                                           const BcSpec& bc, int face, int i1, int i2) {
     const int a = face >> 1, side = face & 1;
     int oth[2], no = 0;
 #pragma unroll
     for (int q = 0; q < D; ++q)
         if (q != a) oth[no++] = q;
-    const long n1 = L.E[oth[0]], n2 = D == 3 ? L.E[oth[1]] : 1;
-    if (t >= n1 * n2) return;
+    if (i1 >= L.E[oth[0]] || (D == 3 ? i2 >= L.E[oth[1]] : i2 > 0)) return;
     int b[3] = {0, 0, 0};
     b[a] = side ? L.B[a] + 1 : 0;
-    if (D == 3) {
-        b[oth[1]] = (int)(t % n2);
-        b[oth[0]] = (int)(t / n2);
-    } else {
-        b[oth[0]] = (int)t;
-    }
+    b[oth[0]] = i1;
+    if (D == 3) b[oth[1]] = i2;
     AxisGeo ax[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -386,19 +381,33 @@ __device__ __forceinline__ void pad_all_pt(double* __restrict__ P, const Lvl& L,
     }
 }
 
+// grid: x over the face's last other axis (3D; 2D: the other axis), y over
+// the first other axis (3D), z = face (+ 2D for the second array of
+// k_pad_all2) -- no integer division
 template <int D>
-__global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, BcSpec bc) {
-    pad_all_pt<D>(P, L, bc, blockIdx.y, blockIdx.x * (long)blockDim.x + threadIdx.x);
+__device__ __forceinline__ void pad_face_coords(int& i1, int& i2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (D == 3) { i1 = blockIdx.y; i2 = i; }
+    else { i1 = i; i2 = 0; }
 }
 
-// the pads of two arrays of one level in one launch (grid.z = 0: P under
-// bc, 1: R under bch) -- the edge tau pass pads p and r together
+template <int D>
+__global__ void __launch_bounds__(TPB) k_pad_all(double* __restrict__ P, Lvl L, BcSpec bc) {
+    int i1, i2;
+    pad_face_coords<D>(i1, i2);
+    pad_all_pt<D>(P, L, bc, blockIdx.z, i1, i2);
+}
+
+// the pads of two arrays of one level in one launch (P under bc, R under
+// bch) -- the edge tau pass pads p and r together
 template <int D>
 __global__ void __launch_bounds__(TPB) k_pad_all2(double* __restrict__ P, BcSpec bc,
                                                   double* __restrict__ R, BcSpec bch, Lvl L) {
-    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (blockIdx.z == 0) pad_all_pt<D>(P, L, bc, blockIdx.y, t);
-    else pad_all_pt<D>(R, L, bch, blockIdx.y, t);
+    int i1, i2;
+    pad_face_coords<D>(i1, i2);
+    const int face = blockIdx.z % (2 * D);
+    if (blockIdx.z < 2 * D) pad_all_pt<D>(P, L, bc, face, i1, i2);
+    else pad_all_pt<D>(R, L, bch, face, i1, i2);
 }
 
 // coarse rows along axis 0 a fine level's blocks restrict to: all m0 of
@@ -1086,40 +1095,43 @@ static bool sweep_mask(Engine& E, int k, unsigned m, const Tile& t) {
         }                                                      \
     } while (0)
 
+// grid of a per-face kernel over (n1 x n2) face positions per face (the
+// largest over the faces), z = nz face slots
+template <int D>
+static dim3 face_grid(const int* ext, int nz, int tpb) {
+    int n1 = 1, n2 = 1;  // first / last other axis, maximised over the faces
+    for (int a = 0; a < D; ++a) {
+        int oth[2], no = 0;
+        for (int t = 0; t < D; ++t)
+            if (t != a) oth[no++] = t;
+        if (D == 3) {
+            n1 = std::max(n1, ext[oth[0]]);
+            n2 = std::max(n2, ext[oth[1]]);
+        } else {
+            n2 = std::max(n2, ext[oth[0]]);
+        }
+    }
+    return dim3((n2 + tpb - 1) / tpb, n1, nz);
+}
+
 template <int D>
 static void launch_pad_fill(Engine& E, int k, long& cnt) {
     const Lvl& L = E.L[k];
-    long face = 1;
-    for (int a = 0; a < D; ++a) face = std::max(face, L.nblk / L.B[a]);
-    dim3 grid(nb(face, 128), 2 * D);
+    const dim3 grid = face_grid<D>(L.B, 2 * D, 128);
     EA_DISPATCH(D, E.ea, (k_pad_fill<D, EA><<<grid, 128, 0, E.stream>>>(E.P[k], L, E.bc)));
     ++cnt;
 }
 
 template <int D>
 static void launch_pad_all(Engine& E, double* P, const Lvl& L, const BcSpec& bc, long& cnt) {
-    long face = 1;
-    for (int a = 0; a < D; ++a) {
-        long f = 1;
-        for (int t = 0; t < D; ++t)
-            if (t != a) f *= L.E[t];
-        face = std::max(face, f);
-    }
-    k_pad_all<D><<<dim3(nb(face, TPB), 2 * D), TPB, 0, E.stream>>>(P, L, bc);
+    k_pad_all<D><<<face_grid<D>(L.E, 2 * D, TPB), TPB, 0, E.stream>>>(P, L, bc);
     ++cnt;
 }
 
 template <int D>
 static void launch_pad_all2(Engine& E, int k, long& cnt) {
     const Lvl& L = E.L[k];
-    long face = 1;
-    for (int a = 0; a < D; ++a) {
-        long f = 1;
-        for (int t = 0; t < D; ++t)
-            if (t != a) f *= L.E[t];
-        face = std::max(face, f);
-    }
-    k_pad_all2<D><<<dim3(nb(face, TPB), 2 * D, 2), TPB, 0, E.stream>>>(E.P[k], E.bc, E.R[k],
+    k_pad_all2<D><<<face_grid<D>(L.E, 4 * D, TPB), TPB, 0, E.stream>>>(E.P[k], E.bc, E.R[k],
                                                                         E.bch, L);
     ++cnt;
 }

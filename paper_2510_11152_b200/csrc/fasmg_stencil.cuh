@@ -156,25 +156,20 @@ __device__ __forceinline__ void push_halo(const PeerHalo& ph, const Lvl& L, int 
 // (2*D faces), x over the face's blocks.
 template <int D, int EA>
 __device__ __forceinline__ void pad_fill_pt(double* __restrict__ P, const Lvl& L,
-                                            const BcSpec& bc, int face, long t) {
+                                            const BcSpec& bc, int face, int i1, int i2) {
     const int a = face >> 1, side = face & 1;
-    // enumerate the other axes' blocks
+    // the other axes' blocks: (i1, i2) 0-based along oth[0], oth[1]
     int oth[2], no = 0;
 #pragma unroll
     for (int t = 0; t < D; ++t)
         if (t != a) oth[no++] = t;
-    long n1 = L.B[oth[0]], n2 = (D == 3) ? L.B[oth[1]] : 1;
-    if (t >= n1 * n2) return;
+    if (i1 >= L.B[oth[0]] || (D == 3 ? i2 >= L.B[oth[1]] : i2 > 0)) return;
     if (a == 0 && ((side == 0 && L.off0 != 0) || (side == 1 && L.off0 + L.B[0] != L.G0)))
         return;  // internal slab face: the halo comes from the neighbor rank
     int bb[3] = {0, 0, 0};
     bb[a] = side ? L.B[a] : 1;
-    if (D == 3) {
-        bb[oth[1]] = 1 + (int)(t % n2);
-        bb[oth[0]] = 1 + (int)(t / n2);
-    } else {
-        bb[oth[0]] = 1 + (int)t;
-    }
+    bb[oth[0]] = 1 + i1;
+    if (D == 3) bb[oth[1]] = 1 + i2;
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
@@ -195,9 +190,13 @@ __device__ __forceinline__ void pad_fill_pt(double* __restrict__ P, const Lvl& L
     }
 }
 
+// grid: x over the face's last other axis (3D; 2D: the other axis), y over
+// the first other axis (3D), z = face -- no integer division
 template <int D, int EA>
 __global__ void k_pad_fill(double* __restrict__ P, Lvl L, BcSpec bc) {
-    pad_fill_pt<D, EA>(P, L, bc, blockIdx.y, blockIdx.x * (long)blockDim.x + threadIdx.x);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (D == 3) pad_fill_pt<D, EA>(P, L, bc, blockIdx.z, blockIdx.y, i);
+    else pad_fill_pt<D, EA>(P, L, bc, blockIdx.z, i, 0);
 }
 
 // ------------------------------------------------------------- smoothing
