@@ -121,6 +121,13 @@ int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, con
 int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, double* scratch,
                    double* sums, double* out, void* stream);
 long fasmg_view_sum_chunks(int dim, const int* ext);
+/* np.sum(vals * vals) of an interior view, the residual norm's sum of
+ * squares (PKG/grid.py:235-249): numpy squares into a contiguous temporary
+ * and sums it with ONE flat pairwise sum; reproduced bitwise.  out[0] on
+ * device; scratch >= fasmg_view_sumsq_scratch() doubles. */
+int fasmg_view_sumsq(const double* v, const long* vs, int dim, const int* ext, double* scratch,
+                     double* out, void* stream);
+long fasmg_view_sumsq_scratch(int dim, const int* ext);
 /* Slab form of the same reduction (SURVEY.md section 8e item v): per-chunk
  * sums of an axis-0 slab `ext` of an interior view whose WHOLE extent is
  * `gext`, with numpy's chunk length for gext (fasmg_view_chunk_len); the

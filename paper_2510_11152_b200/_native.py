@@ -48,6 +48,7 @@ _SIGS = {
     "fasmg_weno_deriv0_3d": "pspsps" + "iiiiii" + "dd" + "S",
     "fasmg_fill_ghosts": "piIiiIDS",
     "fasmg_view_sum": "psiIpppS",
+    "fasmg_view_sumsq": "psiIppS",
     "fasmg_sub_mean": "psiIpdS",
     "fasmg_view_chunk_sums": "psiIIppS",
     "fasmg_chunk_total": "plpS",
@@ -103,6 +104,8 @@ def lib():
         L.fasmg_version.restype = ctypes.c_int
         L.fasmg_view_sum_chunks.argtypes = [ctypes.c_int, _c_int_p]
         L.fasmg_view_sum_chunks.restype = ctypes.c_long
+        L.fasmg_view_sumsq_scratch.argtypes = [ctypes.c_int, _c_int_p]
+        L.fasmg_view_sumsq_scratch.restype = ctypes.c_long
         L.fasmg_view_chunk_len.argtypes = [ctypes.c_int, _c_int_p]
         L.fasmg_view_chunk_len.restype = ctypes.c_long
         L.fasmg_engine_create.argtypes = [
@@ -143,8 +146,20 @@ def check(status: int) -> None:
         raise NativeError(f"libfasmg_b200 error {status}: {msg}")
 
 
+_ctx = threading.local()  # device of the tensors of the call being assembled
+
+
 def call(name: str, *args) -> None:
-    check(getattr(lib(), name)(*args))
+    """Call one C-ABI entry point with the CUDA device of its tensor
+    arguments current (a stream or kernel of another device would be
+    rejected by the runtime)."""
+    dev = getattr(_ctx, "dev", None)
+    _ctx.dev = None
+    if dev is not None and dev.index != torch.cuda.current_device():
+        with torch.cuda.device(dev):
+            check(getattr(lib(), name)(*args))
+    else:
+        check(getattr(lib(), name)(*args))
 
 
 def require_cuda(t: torch.Tensor) -> None:
@@ -155,7 +170,10 @@ def require_cuda(t: torch.Tensor) -> None:
 
 
 def ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    """Device pointer of ``t``; also records t's device for the enclosing
+    :func:`call` and :func:`torch_stream`."""
     require_cuda(t)
+    _ctx.dev = t.device
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -174,9 +192,13 @@ def doubles(seq):
     return (ctypes.c_double * max(len(seq), 1))(*seq)
 
 
-def torch_stream() -> ctypes.c_void_p:
-    """cudaStream_t of torch's current stream."""
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def torch_stream(device=None) -> ctypes.c_void_p:
+    """cudaStream_t of torch's current stream on ``device`` (default: the
+    device of the tensors passed to :func:`ptr` for the call being
+    assembled, else the current device)."""
+    if device is None:
+        device = getattr(_ctx, "dev", None)
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 _streams: dict = {}

@@ -29,6 +29,11 @@ __device__ __forceinline__ bool box_coords(int dim, int e0, int e1, int e2, int*
     x[2] = 0;
     return x[1] < e1 && x[0] < e0;
 }
+// box_grid puts whole array extents on gridDim.y / gridDim.z, which CUDA
+// caps at 65535: callers reject larger boxes with FASMG_EINVAL up front.
+static inline bool box_fits(int dim, int e0, int e1) {
+    return dim == 3 ? (e0 <= 65535 && e1 <= 65535) : e0 <= 65535;
+}
 static inline dim3 box_grid(int dim, int e0, int e1, int e2, int tpb) {
     if (dim == 3) return dim3((unsigned)((e2 + tpb - 1) / tpb), (unsigned)e1, (unsigned)e0);
     return dim3((unsigned)((e1 + tpb - 1) / tpb), (unsigned)e0, 1u);

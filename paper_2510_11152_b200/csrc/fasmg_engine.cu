@@ -1884,6 +1884,13 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
             fasmg_set_error(FASMG_EINVAL, "grid does not stay even through mesh_level coarsenings");
             return nullptr;
         }
+    // launch geometries put (block) extents of the outer axes on gridDim.y/z
+    // (pack_grid, face_grid), which CUDA caps at 65535
+    if ((dim == 3 && (n[0] + 2 > 65535 || n[1] + 2 > 2 * 65535)) ||
+        (dim == 2 && n[0] + 2 > 2 * 65535)) {
+        fasmg_set_error(FASMG_EINVAL, "grid extent exceeds the 65535 CUDA grid-dimension limit");
+        return nullptr;
+    }
     if (nranks < 1 || rank < 0 || rank >= nranks) {
         fasmg_set_error(FASMG_EINVAL, "bad nranks/rank");
         return nullptr;

@@ -550,6 +550,58 @@ __global__ void __launch_bounds__(256) k_chunk_sums_tree(const double* v, S3 vs,
     if (threadIdx.x == 0) sums[c] = leaf[0];
 }
 
+// np.sum(vals * vals) of an interior view (PKG/grid.py:249): numpy squares
+// into a contiguous temporary and runs ONE flat pairwise sum over it.  The
+// split tree (n2 = n/2 rounded down to a multiple of 8, leaves <= 128) is
+// evaluated level by level, deepest first: node t of depth d is found by
+// descending from the root along the bits of t, a leaf squares and sums its
+// elements in numpy's 8-accumulator order, an inner node adds its two
+// children from the level below.  Level d lives at scratch[2^d - 1 + t].
+__device__ __forceinline__ double view_sq(const double* v, S3 vs, int dim, int e1, int e2,
+                                          long q) {
+    long off;
+    if (dim == 2) {
+        off = (q / e1) * vs.s[0] + (q % e1) * vs.s[1];
+    } else {
+        long k = q % e2, r = q / e2;
+        off = (r / e1) * vs.s[0] + (r % e1) * vs.s[1] + k * vs.s[2];
+    }
+    const double x = v[off];
+    return ml(x, x);
+}
+
+__global__ void k_pw_sumsq_level(const double* v, S3 vs, int dim, int e1, int e2, long n, int d,
+                                 double* scratch) {
+    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (t >= (1L << d)) return;
+    long off = 0, len = n;
+    for (int b = d - 1; b >= 0; --b) {
+        if (len <= 128) return;  // a leaf above this depth: no node here
+        long n2 = len / 2;
+        n2 -= n2 % 8;
+        if ((t >> b) & 1) { off += n2; len -= n2; } else { len = n2; }
+    }
+    double res;
+    if (len > 128) {
+        const double* lo = scratch + (1L << (d + 1)) - 1;
+        res = ad(lo[2 * t], lo[2 * t + 1]);
+    } else if (len < 8) {
+        res = 0.;
+        for (long i = 0; i < len; ++i) res = ad(res, view_sq(v, vs, dim, e1, e2, off + i));
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = view_sq(v, vs, dim, e1, e2, off + j);
+        long i;
+        for (i = 8; i < len - (len % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = ad(r[j], view_sq(v, vs, dim, e1, e2, off + i + j));
+        res = ad(ad(ad(r[0], r[1]), ad(r[2], r[3])), ad(ad(r[4], r[5]), ad(r[6], r[7])));
+        for (; i < len; ++i) res = ad(res, view_sq(v, vs, dim, e1, e2, off + i));
+    }
+    scratch[(1L << d) - 1 + t] = res;
+}
+
 __global__ void k_chunk_total(const double* sums, long nchunks, double* out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double acc = 0.0;
@@ -1035,6 +1087,48 @@ int fasmg_view_sum(const double* v, const long* vs, int dim, const int* ext, dou
     return fasmg_chunk_total(sums, nch, out, stream);
 }
 
+// depth of numpy's pairwise split tree over n elements (its deepest leaf
+// lies on the always-right path, whose node sizes are the largest)
+static int pw_depth(long n) {
+    int d = 0;
+    while (n > 128) {
+        long n2 = n / 2;
+        n2 -= n2 % 8;
+        n -= n2;
+        ++d;
+    }
+    return d;
+}
+
+// doubles of scratch fasmg_view_sumsq needs for a view of extent ext
+long fasmg_view_sumsq_scratch(int dim, const int* ext) {
+    long n = 1;
+    for (int a = 0; a < dim; ++a) n *= ext[a];
+    return (2L << pw_depth(n)) - 1;
+}
+
+// out[0] = np.sum(v * v) over a C-order interior view, numpy's flat pairwise
+// order (bitwise); scratch holds fasmg_view_sumsq_scratch doubles
+int fasmg_view_sumsq(const double* v, const long* vs, int dim, const int* ext, double* scratch,
+                     double* out, void* stream) {
+    if (dim != 2 && dim != 3) return fasmg_set_error(FASMG_EINVAL, "dim must be 2 or 3");
+    long n = 1;
+    for (int a = 0; a < dim; ++a) n *= ext[a];
+    S3 s = mk(vs);
+    if (dim == 2) s.s[2] = 0;
+    if (n == 0) return fasmg_check(cudaMemsetAsync(out, 0, sizeof(double), S(stream)));
+    const int D = pw_depth(n);
+    for (int d = D; d >= 0; --d) {
+        const long cnt = 1L << d;
+        k_pw_sumsq_level<<<nblk(cnt, 128), 128, 0, S(stream)>>>(v, s, dim, ext[1],
+                                                                dim == 3 ? ext[2] : 1, n, d,
+                                                                scratch);
+        if (int st = fasmg_check_launch()) return st;
+    }
+    return fasmg_check(cudaMemcpyAsync(out, scratch, sizeof(double), cudaMemcpyDeviceToDevice,
+                                       S(stream)));
+}
+
 long fasmg_view_sum_chunks(int dim, const int* ext) {
     long n = 1;
     for (int a = 0; a < dim; ++a) n *= ext[a];
@@ -1080,6 +1174,7 @@ int fasmg_divergence(const double* const* comps, const long* cs, double* out, co
     }
     S3 o = mk(os);
     if (dim == 2) o.s[2] = 0;
+    if (!box_fits(dim, n[0], n[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
     long tot = (long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
     LAUNCH(tot, (k_div<<<box_grid(dim, n[0], n[1], dim == 3 ? n[2] : 1, 128), 128, 0,
                          S(stream)>>>(C, out, o, dim, n[0], n[1], dim == 3 ? n[2] : 1, inv_h)));
@@ -1097,6 +1192,7 @@ int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
     }
     S3 o = mk(os);
     if (dim == 2) o.s[2] = 0;
+    if (!box_fits(dim, ext[0], ext[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
     long tot = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
     LAUNCH(tot, (k_ns_elem<<<box_grid(dim, ext[0], ext[1], dim == 3 ? ext[2] : 1, 128), 128, 0,
                              S(stream)>>>(op, out, o, v, s0, s1, dim, ext[0], ext[1],
@@ -1112,6 +1208,7 @@ int fasmg_ns_rhs(int order, double* out, const long* os, const double* ucore, co
                  double inv_h2, void* stream) {
     S3 o = mk(os), uu = mk(us), cc = mk(cs), pp = mk(ps);
     if (dim == 2) { o.s[2] = 0; uu.s[2] = 0; cc.s[2] = 0; pp.s[2] = 0; }
+    if (!box_fits(dim, m[0], m[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
     long tot = (long)m[0] * m[1] * (dim == 3 ? m[2] : 1);
     LAUNCH(tot, (k_ns_rhs<<<box_grid(dim, m[0], m[1], dim == 3 ? m[2] : 1, 128), 128, 0,
                             S(stream)>>>(

@@ -94,21 +94,31 @@ class _Engine:
         except Exception:
             pass
 
+    def _same_device(self, *fields):
+        for F in fields:
+            if F.device != self.device:
+                raise ValueError(f"field on {F.device}, solver engine on {self.device}")
+
     def load(self, p: Field, f: Field):
-        N.wait(self.stream, N.torch_stream())
-        pc, fc = p.core, f.core
-        N.call("fasmg_engine_load", self.handle, N.ptr(pc), N.strides(pc), N.ptr(fc),
-               N.strides(fc))
+        self._same_device(p, f)
+        with torch.cuda.device(self.device):
+            N.wait(self.stream, N.torch_stream(self.device))
+            pc, fc = p.core, f.core
+            N.call("fasmg_engine_load", self.handle, N.ptr(pc), N.strides(pc), N.ptr(fc),
+                   N.strides(fc))
 
     def store(self, p: Field):
-        pc = p.core
-        N.call("fasmg_engine_store", self.handle, N.ptr(pc), N.strides(pc))
-        N.wait(N.torch_stream(), self.stream)
+        self._same_device(p)
+        with torch.cuda.device(self.device):
+            pc = p.core
+            N.call("fasmg_engine_store", self.handle, N.ptr(pc), N.strides(pc))
+            N.wait(N.torch_stream(self.device), self.stream)
 
     def run(self, count: int, with_norm: bool, use_graph: bool = True) -> float:
         out = ctypes.c_double(0.0)
-        N.call("fasmg_engine_run", self.handle, int(count), 1 if with_norm else 0,
-               ctypes.byref(out), 1 if use_graph else 0)
+        with torch.cuda.device(self.device):
+            N.call("fasmg_engine_run", self.handle, int(count), 1 if with_norm else 0,
+                   ctypes.byref(out), 1 if use_graph else 0)
         return out.value
 
     def kernels_per_vcycle(self, with_norm: bool = True) -> int:
@@ -119,7 +129,9 @@ class _Engine:
         """Mean duration (ms) of one smoothing half-sweep launch on `level`,
         CUDA events on the engine stream."""
         ms = ctypes.c_double()
-        N.call("fasmg_engine_time_sweeps", self.handle, int(level), int(reps), ctypes.byref(ms))
+        with torch.cuda.device(self.device):
+            N.call("fasmg_engine_time_sweeps", self.handle, int(level), int(reps),
+                   ctypes.byref(ms))
         return ms.value
 
 
@@ -198,6 +210,12 @@ class FasSolver:
         For a singular problem the rhs is shifted to zero mean in place and
         the returned solution is shifted to zero mean."""
         self._check(p, f)
+        with torch.cuda.device(p.device):
+            history = self._solve(p, f, params)
+        return SolveReport(iterations=len(history), residual_history=history,
+                           converged=bool(history and history[-1] <= params.tol))
+
+    def _solve(self, p: Field, f: Field, params: FasParams) -> list:
         singular = self._singular()
         if singular:
             subtract_interior_mean(f)
@@ -217,8 +235,7 @@ class FasSolver:
         if singular:
             subtract_interior_mean(p)
             p.ghosts_fresh = False
-        return SolveReport(iterations=len(history), residual_history=history,
-                           converged=bool(history and history[-1] <= params.tol))
+        return history
 
     # -- independent problems held in host memory --------------------------
     def solve_host_batch(self, ps, fs, params: FasParams, out=None, halo: int = 1,
@@ -241,10 +258,37 @@ class FasSolver:
         n = len(ps)
         if len(fs) != n or (out is not None and len(out) != n):
             raise ValueError("ps, fs and out must have the same length")
+        if n == 0:
+            return []
         out = list(ps) if out is None else list(out)
         dev = torch.device(device) if device is not None else \
             torch.device("cuda", torch.cuda.current_device())
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         g = self.hierarchy.fine
+        singular = self._singular()
+        # reject a result that would be copied out while memory it overlaps is
+        # still to be read (the input of another problem, or -- singular
+        # problems write the shifted rhs back -- a written array of any problem)
+        spans = [(_host_span(t), j % n, j < n) for j, t in enumerate((*ps, *fs))]
+        written = [(_host_span(t), i) for i, t in enumerate(out)]
+        if singular:
+            written += [(_host_span(t), i) for i, t in enumerate(fs)]
+        for w, i in written:
+            for r, j, _ in spans:
+                if j != i and _overlap(w, r):
+                    raise ValueError(f"a written host array of problem {i} shares memory with "
+                                     f"the input of problem {j}")
+        if singular:
+            for i in range(n):
+                if _overlap(_host_span(out[i]), _host_span(fs[i])):
+                    raise ValueError(f"problem {i}: out shares memory with f, which a singular "
+                                     "solve writes back shifted")
+        with torch.cuda.device(dev):
+            return self._host_batch(ps, fs, out, params, halo, dev, g, singular)
+
+    def _host_batch(self, ps, fs, out, params, halo, dev, g, singular) -> list:
+        n = len(ps)
         # two staging (p, f) pairs per (device, halo), kept on the solver so
         # that repeated batches allocate nothing
         bufs = self._staging.setdefault((dev.index, halo), [])
@@ -256,17 +300,6 @@ class FasSolver:
         for t in (*ps, *fs, *out):
             if t.device.type != "cpu" or tuple(t.shape) != shape or t.dtype != torch.float64:
                 raise ValueError(f"host arrays must be float64 CPU tensors of shape {shape}")
-        # a result copied out while another problem's input is read from the
-        # same host memory would race (the copies overlap by design)
-        ins = {}
-        for j, t in enumerate((*ps, *fs)):
-            ins.setdefault(t.data_ptr(), set()).add(j % n)
-        written = list(out) + (list(fs) if self._singular() else [])  # singular: f is shifted
-        for i, t in enumerate(written):
-            if ins.get(t.data_ptr(), {i % n}) - {i % n}:
-                raise ValueError(f"a written host array of problem {i % n} shares memory with "
-                                 "the input of another problem")
-        singular = self._singular()
         comp = torch.cuda.current_stream(dev)
         h2d = torch.cuda.Stream(dev)
         d2h = torch.cuda.Stream(dev)
@@ -285,8 +318,7 @@ class FasSolver:
 
         reports = []
         h2d.wait_stream(comp)  # earlier work on the staging buffers was ordered on comp
-        if n:
-            enqueue_h2d(0)
+        enqueue_h2d(0)
         for i in range(n):
             if i + 1 < n:
                 enqueue_h2d(i + 1)
@@ -306,7 +338,22 @@ class FasSolver:
                 drained[b].record(d2h)
         comp.wait_stream(d2h)
         comp.wait_stream(h2d)
+        # the results are in host memory when this returns: the last copies
+        # out are still in flight on d2h until here
+        d2h.synchronize()
         return reports
+
+
+def _host_span(t: torch.Tensor):
+    """(storage address, first byte, end byte) of a host tensor's data."""
+    st = t.untyped_storage()
+    lo = t.storage_offset() * t.element_size()
+    ext = 1 + sum((m - 1) * abs(s) for m, s in zip(t.shape, t.stride())) if t.numel() else 0
+    return st.data_ptr(), st.data_ptr() + lo, st.data_ptr() + lo + ext * t.element_size()
+
+
+def _overlap(a, b) -> bool:
+    return a[1] < b[2] and b[1] < a[2]
 
 
 def vcycle(p: Field, f: Field, coeffs: OperatorCoeffs, params: FasParams,

@@ -325,3 +325,32 @@ def solve_inputs(c, manufactured=None):
     else:
         f[isl] = manufactured(c["rhs"], n)
     return p, f
+
+
+# ---- round-2 golden set (make_golden_r2.py -> golden_r2.npz) ----
+NS_CASES = [
+    dict(n=(16, 16), order=1, re=100.0, dt=1e-2, steps=3),
+    dict(n=(16, 16), order=2, re=100.0, dt=1e-2, steps=3),
+    dict(n=(8, 8, 8), order=1, re=100.0, dt=1e-2, steps=3),
+    dict(n=(8, 8, 8), order=2, re=100.0, dt=1e-2, steps=3),
+    dict(n=(16, 16, 16), order=2, re=100.0, dt=1e-3, steps=2),
+]
+
+DENSE_CASES = [
+    dict(n=(4, 4), loc="cell", bc=bc, a=1.0, b=0.5) for bc in BCS
+] + [
+    dict(n=(4, 4), loc="edge_ew", bc="lid", a=1.0, b=0.25),
+    dict(n=(4, 4), loc="edge_ns", bc="mixed", a=1.0, b=0.25),
+    dict(n=(4, 4, 4), loc="cell", bc="neumann", a=0.0, b=1.0),
+    dict(n=(4, 4, 4), loc="edge_tb", bc="lid", a=1.0, b=0.1),
+    dict(n=(4, 4, 4), loc="edge_ew", bc="periodic", a=1.0, b=0.1),
+]
+
+
+def ns_key(c):
+    return "ns/{}_o{}_dt{:g}".format("x".join(map(str, c["n"])), c["order"], c["dt"])
+
+
+def dense_key(c):
+    return "dense/{}_{}_{}_a{:g}_b{:g}".format("x".join(map(str, c["n"])), c["loc"], c["bc"],
+                                               c["a"], c["b"])

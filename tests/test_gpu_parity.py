@@ -212,3 +212,54 @@ def test_view_sum_tree_and_serial_paths(P, shape):
     inner = tuple(slice(1, s - 1) for s in shape)
     got = float(view_sum(dev(a)[inner]).item())
     assert got == float(O.view_sum(a[inner]))
+
+
+@pytest.mark.parametrize("c", cases("weno"), ids=lambda c: c["key"])
+def test_weno3_convect_api(P, c):
+    """The public weno3_convect (fused one-pass kernel) against the
+    reference's weno3_convect on the same halo-2 velocities, bitwise."""
+    n = tuple(c["n"])
+    g = P.unit_grid(n)
+    locs = ("edge_ew", "edge_ns", "edge_tb")[: c["dim"]]
+    vel = []
+    for t, loc in enumerate(locs):
+        F = P.Field(g, loc_of(P, loc), 2, C.rand_field(c["seed"] + 10 * t, n, loc, 2))
+        F.ghosts_fresh = True
+        vel.append(F)
+    res = P.weno3_convect(tuple(vel), c["target"])
+    expect_array(f"{c['key']}/conv", host(res.interior))
+    assert not res.ghosts_fresh
+
+
+@pytest.mark.parametrize("c", cases("reduce"), ids=lambda c: c["key"])
+def test_norm_l2_scaled_numpy_order(P, c):
+    """The public norm_l2_scaled sums squares in numpy's flat pairwise
+    order: the sum of squares is the reference's bitwise, on a Field and on
+    a bare device array."""
+    G = golden()
+    a = np.random.default_rng(c["seed"]).standard_normal(c["shape"])
+    t = dev(a)
+    v = t[tuple(slice(1, s - 1) for s in c["shape"])]
+    from paper_2510_11152_b200.grid import view_sumsq
+    assert float(view_sumsq(v).item()) == float(G[f"{c['key']}/sumsq"])
+    n = tuple(s - 2 for s in c["shape"])
+    g = P.GridLevel(0, n, (0.0,) * len(n), tuple(x / n[-1] for x in n))
+    F = P.Field(g, P.Location.CELL, 1, a)
+    ref = g.h ** (g.dim / 2.0) * np.sqrt(float(G[f"{c['key']}/sumsq"]))
+    assert P.norm_l2_scaled(F) == ref
+    assert P.norm_l2_scaled(v, g) == ref
+
+
+@pytest.mark.parametrize("c", C.DENSE_CASES, ids=C.dense_key)
+def test_assemble_dense_operator(P, c):
+    """stencil.assemble_dense_operator (probed from the device operator)
+    against the reference's row-wise assembly (PKG/stencil.py:172-215)."""
+    from paper_2510_11152_b200.stencil import assemble_dense_operator
+    dim = len(c["n"])
+    g = P.unit_grid(tuple(c["n"]))
+    mat = assemble_dense_operator(g, loc_of(P, c["loc"]), P.OperatorCoeffs(c["a"], c["b"]),
+                                  bc_of(P, dim, c["bc"]))
+    ref = golden()[C.dense_key(c)]
+    assert mat.shape == ref.shape
+    np.testing.assert_allclose(mat, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+    assert np.array_equal(mat != 0, ref != 0)

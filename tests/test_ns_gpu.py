@@ -105,3 +105,77 @@ def test_weno_fused_equals_per_axis(P, dim, n):
         a = weno3_convect(tuple(vel), t, fused=True).interior.cpu().numpy()
         b = weno3_convect(tuple(vel), t, fused=False).interior.cpu().numpy()
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), t
+
+
+@pytest.mark.parametrize("c", __import__("cases").NS_CASES, ids=__import__("cases").ns_key)
+def test_ns_matches_reference_composition(P, c):
+    """GPU stepper against projection steps composed from the REAL reference
+    primitives (tests/golden/make_golden_r2.py): histories within 1e-10,
+    velocity (with ghosts) and pressure fields bitwise, every step."""
+    from _golden import expect_array, golden
+    import cases as C
+    G = golden()
+    key = C.ns_key(c)
+    st = _stepper(P, tuple(c["n"]), c["order"], "efficient", dt=c["dt"], re=c["re"])
+    for s in range(c["steps"]):
+        rep = st.step()
+        for k in st.comps:
+            np.testing.assert_allclose(rep.momentum[k].residual_history,
+                                       G[f"{key}/s{s}/hist_{k}"], rtol=1e-10, atol=0)
+        np.testing.assert_allclose(rep.pressure.residual_history, G[f"{key}/s{s}/hist_p"],
+                                   rtol=1e-10, atol=0)
+        for k in st.comps:
+            expect_array(f"{key}/s{s}/{k}", st.velocity(k).numpy())
+        expect_array(f"{key}/s{s}/p", st.pressure().interior.cpu().numpy())
+
+
+def _host_mem_gb():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    return 0.0
+
+
+@pytest.mark.slow
+def test_ns_512_config4_matches_oracle(P):
+    """BASELINE.json configs[3] at full size: 3D lid-driven cavity 512^3,
+    second-order projection, memory-efficient 8-slot schedule, Re 100,
+    dt 1e-3, tol 1e-10, kMax 20, s 2, meshLevel 8.  Two steps on the GPU
+    against the pinned NS oracle (oracle/ns_oracle.py, C kernels on all host
+    threads): every momentum/pressure residual history within 1e-10 and
+    the velocity and pressure fields bitwise after each step."""
+    import os
+    import ns_oracle as NO
+    import oracle as O
+    if _host_mem_gb() < 40:
+        pytest.skip(f"the 512^3 CPU oracle needs ~30 GB of host RAM ({_host_mem_gb():.0f} GB free)")
+    n = (512, 512, 512)
+    from paper_2510_11152_b200.ns import NSParams, ProjectionStepper
+    st = ProjectionStepper(P.unit_grid(n), NSParams(re=100.0, dt=1e-3, order=2, mode="efficient",
+                                                    tol=1e-10, k_max=20, s=2, mesh_level=8))
+    st.set_state({})
+    O.set_threads(len(os.sched_getaffinity(0)))
+    orc = NO.NSOracle(n, 100.0, 1e-3, 2, tol=1e-10, k_max=20, s=2, mesh_level=8)
+    try:
+        for k in range(2):
+            rep = st.step()
+            hist = orc.step()
+            for c in st.comps:
+                np.testing.assert_allclose(rep.momentum[c].residual_history, hist[c],
+                                           rtol=1e-10, atol=0)
+            np.testing.assert_allclose(rep.pressure.residual_history, hist["p"], rtol=1e-10,
+                                       atol=0)
+            for c in st.comps:
+                got = st.velocity(c).data
+                ref = torch.from_numpy(orc.un[c].data).to(got.device)
+                assert torch.equal(got.view(torch.int64), ref.view(torch.int64)), (k, c)
+                del ref
+            gp = st.pressure().interior
+            ref = torch.from_numpy(np.ascontiguousarray(orc.p.interior)).to(gp.device)
+            assert torch.equal(gp.contiguous().view(torch.int64), ref.view(torch.int64)), k
+            del ref
+    finally:
+        O.set_threads(1)

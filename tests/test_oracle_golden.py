@@ -117,3 +117,21 @@ def test_paper_asymptotic_3d_32():
     assert float(np.max(np.abs(e))) == float(golden()[f"{c['key']}/err_max"])
     err = (1.0 / 32) ** 1.5 * np.sqrt(np.sum(e * e))  # scaled L2 error
     assert abs(err - 1.74e-3) / 1.74e-3 < 0.01
+
+
+@pytest.mark.parametrize("c", C.NS_CASES, ids=C.ns_key)
+def test_ns_oracle_vs_reference_composition(c):
+    """oracle/ns_oracle.py against projection steps composed from the REAL
+    reference primitives (tests/golden/make_golden_r2.py): residual
+    histories and fields bitwise, step by step."""
+    import ns_oracle as NO
+    G = golden()
+    key = C.ns_key(c)
+    orc = NO.NSOracle(tuple(c["n"]), c["re"], c["dt"], c["order"])
+    for s in range(c["steps"]):
+        hist = orc.step()
+        for k in orc.comps + ("p",):
+            assert hist[k] == G[f"{key}/s{s}/hist_{k}"].tolist(), (s, k)
+        for k in orc.comps:
+            expect_array(f"{key}/s{s}/{k}", orc.un[k].data)
+        expect_array(f"{key}/s{s}/p", orc.p.interior)
