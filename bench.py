@@ -32,8 +32,18 @@ test -- the paper's per-"iteration" time.
   this half of f, write this half of p).
 * cpu_baseline: the CPU oracle port of the reference (oracle/, C, all host
   threads) timed on one V-cycle + norm of the same inputs, rank 0, N = 1.
-* --impl reference: the same metric from the oracle port alone (the
-  reference is pure Python+numba and does not travel to the GPU box).
+* cpu_baseline_reference_1core: the UNMODIFIED reference package
+  (baseline/_ref, numba backend, NUMBA_NUM_THREADS=1 -- its parallel
+  Gauss-Seidel is unusable) timed on one outer
+  iteration of the same inputs in a subprocess: the paper's own
+  single-core baseline configuration.
+* --impl reference: the same metric, config, K and W from the oracle port
+  alone on all host threads.
+* --workload ns512|ns1024: one Navier-Stokes projection step (BASELINE
+  configs[3]/[4]) per bench step: steps/s, per-solve MDOF/s per V-cycle,
+  the edge-field half-sweep against the roofline.
+* --gpus N > 1 outside torchrun relaunches itself under
+  torch.distributed.run with N processes.
 
 Multi-GPU (torchrun, one process per GPU): the SAME 512^3 problem is split
 into axis-0 slabs (paper_2510_11152_b200/slab.py DistSlabSolver): halo
@@ -73,6 +83,12 @@ def parse():
     ap.add_argument("--dim", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--workload", default="heat", choices=("heat", "ns512", "ns1024", "ns"),
+                    help="heat: the headline V-cycle metric; ns512/ns1024: one Navier-Stokes "
+                         "projection step of BASELINE configs[3]/[4] per bench step")
+    ap.add_argument("--no-numba-baseline", action="store_true",
+                    help="skip the single-core run of the real reference (baseline/_ref)")
+    ap.add_argument("--numba-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -96,7 +112,13 @@ def config_dict(n, dim, parallelism):
                      else "none: each field is %.3f GB, not >> 126 MB L2 (functional size, not a "
                           "bench configuration)" % (fb / 1e9)),
         "parallelism": parallelism,
+        "pack_unpack": "excluded from value (p and f stay in the engine's parity-blocked "
+                       "layout between steps), included in e2e",
     }
+
+
+def parallelism_of(world: int) -> str:
+    return "single" if world == 1 else f"z-slab x{world}"
 
 
 def make_inputs(n, dim):
@@ -211,9 +233,15 @@ def host_threads():
 
 # --------------------------------------------------------------- reference arm
 def reference_arm(args):
+    """The reference's CPU path on the box's host cores: the oracle/ C port of
+    the reference V-cycle (pinned bitwise to the reference's own outputs) on
+    all host threads, W warm-up steps then K timed steps of the SAME
+    workload and config as the GPU arm.  Rank 0 only under torchrun."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    if args.workload != "heat":
+        return ns_reference_arm(args)
     n, dim = args.n, args.dim
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
@@ -222,18 +250,20 @@ def reference_arm(args):
     p0[(slice(1, -1),) * dim] = np.random.default_rng(0).random((n,) * dim)
     f_int = O.poisson_rhs_discrete((n,) * dim)
     threads = host_threads()
-    budget_s = 150.0
-    t_first = cpu_oracle_vcycle(p0, f_int, n, dim, threads)  # warm-up step (also a sample)
-    steps = max(1, min(args.steps, int(budget_s / max(t_first, 1e-3))))
+    K, W = args.steps, max(args.warmup, 3)
+    t_w = cpu_oracle_vcycle(p0, f_int, n, dim, threads, cycles=W)  # warm-up steps
+    budget_s = 240.0
+    steps = K if t_w * K <= budget_s else max(1, int(budget_s / max(t_w, 1e-3)))
     t = cpu_oracle_vcycle(p0, f_int, n, dim, threads, cycles=steps)
     value = n ** dim / t / 1e6
-    sample = (f"{steps} V-cycle(s)+norm of the full {n}^{dim} workload after 1 warm-up cycle, "
-              f"oracle/ C port of the reference, OpenMP {threads} threads")
+    sample = (f"{steps} V-cycle(s)+norm of the full {n}^{dim} workload after {W} warm-up "
+              f"cycles, oracle/ C port of the reference, OpenMP {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MDOF/s",
-        "n_gpus": world, "steps": steps, "warmup": 1, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(n, dim, "cpu"),
+        "n_gpus": world, "steps": steps, "warmup": W, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(n, dim, parallelism_of(world)),
         "cpu_baseline": {"value": value, "unit": "MDOF/s", "cores": threads, "kind": "port",
                          "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "MDOF/s", "h2d_bytes_per_step": 0,
@@ -244,6 +274,70 @@ def reference_arm(args):
     return 0
 
 
+# ------------------------------------------- the real reference, one core
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def numba_child(args):
+    """Runs in a subprocess with NUMBA_NUM_THREADS=1 and baseline/_ref on the
+    path: the UNMODIFIED reference package (numba backend) times one outer
+    iteration (V-cycle + residual norm, FasSolver.solve with kMax=1) of the
+    same workload after a JIT warm-up on a 16^d grid; prints one JSON line."""
+    import fasmg as fm
+    from fasmg import manufactured as M
+    n, dim = args.n, args.dim
+    ml = int(np.log2(n)) - 1
+
+    def problem(m):
+        g = fm.unit_grid((m,) * dim)
+        p = fm.Field(g, fm.Location.CELL, 1)
+        p.interior[...] = np.random.default_rng(0).random((m,) * dim)
+        f = M.poisson_rhs_discrete(g)
+        S = fm.FasSolver(fm.make_hierarchy(g, int(np.log2(m)) - 1), fm.Location.CELL,
+                         fm.BoundaryCondition.dirichlet(dim), fm.make_plan("x", dim, "ff"),
+                         fm.OperatorCoeffs(1.0, 1.0))
+        return p, f, S
+
+    t0 = time.perf_counter()
+    p, f, S = problem(16)
+    S.solve(p, f, fm.FasParams(1e-300, 2, 2, 3))  # JIT compile
+    t_jit = time.perf_counter() - t0
+    p, f, S = problem(n)
+    t0 = time.perf_counter()
+    rep = S.solve(p, f, fm.FasParams(1e-300, 1, 2, ml))
+    t = time.perf_counter() - t0
+    print(json.dumps({"s_per_step": t, "jit_s": t_jit, "residual": rep.residual_history[-1],
+                      "backend": os.environ.get("FASMG_BACKEND", "numba"),
+                      "numba_threads": os.environ.get("NUMBA_NUM_THREADS")}), flush=True)
+    return 0
+
+
+def numba_baseline(n, dim):
+    """Single-core timing of the real reference (the
+    numba backend, 1 core -- its parallel Gauss-Seidel is unusable, SURVEY.md
+    section 0 item 2) or None when baseline/_ref is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "fasmg")):
+        return None
+    env = dict(os.environ, NUMBA_NUM_THREADS="1", OMP_NUM_THREADS="1",
+               NUMBA_CACHE_DIR="/tmp/fasmg_numba_cache", PYTHONDONTWRITEBYTECODE="1",
+               PYTHONPATH=REF_DIR + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(k, None)
+    try:
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--numba-child",
+                              "--grid", str(n), "--dim", str(dim)], env=env,
+                             capture_output=True, text=True, timeout=600)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 -- reported, never fatal to the GPU line
+        return {"unavailable": f"{type(e).__name__}: {str(e)[:200]}"}
+    t = d["s_per_step"]
+    return {"value": n ** dim / t / 1e6, "unit": "MDOF/s", "cores": 1, "kind": "reference",
+            "sample": f"1 V-cycle + residual norm (FasSolver.solve, kMax=1) of the same {n}^{dim} "
+                      "inputs by the unmodified reference package (baseline/_ref, numba "
+                      "backend, NUMBA_NUM_THREADS=1) after a 16^d JIT warm-up",
+            "s_per_step": t, "cpu": cpu_model()}
+
+
 # ------------------------------------------------------------------ B200 arm
 def b200_arm(args):
     import torch
@@ -251,8 +345,6 @@ def b200_arm(args):
     from paper_2510_11152_b200.grid import Field, Location
 
     rank, world, local = dist_env()
-    if world != args.gpus and rank == 0:
-        print(f"[bench] warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
     ndev = torch.cuda.device_count()
     shared = world > ndev  # functional test: several ranks on one device
     dev = torch.device("cuda", local % ndev)
@@ -293,7 +385,7 @@ def b200_arm(args):
         run_step = lambda: eng.run(1, with_norm=True)  # noqa: E731
         stream_handle = eng.stream.value
         local_dof = dof
-        parallelism = "single"
+        slab_detail = None
     else:
         from paper_2510_11152_b200.slab import DistSlabSolver, slab_view
         ds = DistSlabSolver(hier, Location.CELL, bc, plan, coeffs, 2, dev)
@@ -309,8 +401,8 @@ def b200_arm(args):
             return eng.result()
         stream_handle = eng.stream.value
         local_dof = dof // world
-        parallelism = (f"z-slab x{world} (axis-0 slabs, halo push per half-sweep over "
-                       f"CUDA IPC/NVLink, coarse levels >= {eng.kg} gathered)"
+        slab_detail = (f"axis-0 slabs, halo push per half-sweep over CUDA IPC/NVLink, "
+                       f"coarse levels >= {eng.kg} gathered"
                        + (" [ranks sharing one device: functional test only]" if shared else ""))
     torch.cuda.synchronize()
 
@@ -480,6 +572,9 @@ def b200_arm(args):
                "sample": f"1 V-cycle + residual norm of the same {n}^{dim} inputs on the oracle/ "
                          f"C port of the reference (OpenMP, {threads} threads)",
                "cpu": cpu_model(), "s_per_step": t_cpu}
+    numba = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_numba_baseline:
+        numba = numba_baseline(n, dim)
 
     if rank == 0:
         line = {
@@ -489,8 +584,10 @@ def b200_arm(args):
             "vs_baseline": value / PAPER_4090_MDOFS,
             "vs_baseline_ref": "RTX 4090, 0.4633 s per V-cycle at 3D 512^3 (PAPER.md:510)",
             "dtype": "f64", "data": "synthetic",
-            "config": config_dict(n, dim, parallelism),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": config_dict(n, dim, parallelism_of(world)),
+            "slab": slab_detail,
+            "roofline": roofline, "cpu_baseline": cpu,
+            "cpu_baseline_reference_1core": numba, "e2e": e2e,
             "clocks": clocks.summary(), "gpu_launches": kernels * K,
             "kernels_per_step": kernels,
             "residual_last": (g.h ** (dim / 2.0)) * float(np.sqrt(hist[-1])) if hist else None,
@@ -504,10 +601,210 @@ def b200_arm(args):
     return 0
 
 
+# ---------------------------------------------------- Navier-Stokes workload
+NS_METRIC = "NS projection steps/s, 3D lid-driven cavity {n}³, 2nd order, 8-slot schedule (f64)"
+
+
+def ns_config(n, world):
+    ml = int(np.log2(n)) - 1
+    return {
+        "workload": f"ns3d_{n}: lid-driven cavity (u=1 on zhi), Re 100, dt 1e-3, 2nd-order MAC "
+                    f"projection, memory-efficient 8-slot schedule (PAPER.md Table 5), FAS "
+                    f"X-MCGS ff s=2 tol 1e-10 kMax 20 meshLevel {ml}, from rest after the "
+                    f"warm-up steps",
+        "grid": [n] * 3, "mesh_level": ml, "order": 2, "schedule": "efficient (8 slots)",
+        "step": "one projection step: 3 momentum rhs (WENO3) + 3 edge-field FAS solves + "
+                "divergence + singular pressure FAS solve + correction + p update",
+        "l2_flush": "not needed: each field is %.2f GB >> 126 MB L2" % ((n + 2) ** 3 * 8 / 1e9),
+        "parallelism": parallelism_of(world),
+        "pack_unpack": "included (each solve packs p, f into the blocked layout and unpacks p)",
+    }
+
+
+def ns_size(args):
+    return {"ns512": 512, "ns1024": 1024}.get(args.workload, args.n)
+
+
+def ns_arm(args):
+    """One NS projection step per bench step (BASELINE configs[3] at 512^3,
+    configs[4] at 1024^3), single GPU: steps/s, per-solve MDOF/s per V-cycle
+    from CUDA events around every schedule Step, the edge-field finest
+    half-sweep against the HBM roofline."""
+    import torch
+    import paper_2510_11152_b200 as P
+    from paper_2510_11152_b200.ns import NSParams, ProjectionStepper
+
+    rank, world, local = dist_env()
+    if world > 1:
+        print(json.dumps({"metric": NS_METRIC.format(n=ns_size(args)),
+                          "unavailable": "multi-GPU NS runs through scripts/ns_slab_bench.py"}))
+        return 0
+    n = ns_size(args)
+    K, W = args.steps, max(args.warmup, 3)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    ml = int(np.log2(n)) - 1
+    st = ProjectionStepper(P.unit_grid((n,) * 3), NSParams(re=100.0, dt=1e-3, order=2,
+                                                           mode="efficient", tol=1e-10, k_max=20,
+                                                           s=2, mesh_level=ml), device=dev)
+    st.set_state({})
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    for _ in range(W):
+        st.step()
+    torch.cuda.synchronize()
+    st.timing = []
+    cur = torch.cuda.current_stream(dev)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
+    a.record(cur)
+    reps = [st.step() for _ in range(K)]
+    b.record(cur)
+    torch.cuda.synchronize()
+    clocks.mark(t0, time.time())
+    ms_step = a.elapsed_time(b) / K
+    # per formula/component device time, and V-cycles per solve
+    per = {}
+    for formula, comp, e0, e1 in st.timing:
+        key = formula if formula in ("copy", "rotate2", "p_update") else f"{formula}:{comp or 'p'}"
+        per[key] = per.get(key, 0.0) + e0.elapsed_time(e1) / K
+    st.timing = None
+    cyc = {c: sum(r.momentum[c].iterations for r in reps) / K for c in st.comps}
+    cyc["p"] = sum(r.pressure.iterations for r in reps) / K
+    solves = {}
+    for c in st.comps + ("p",):
+        key = f"solve_momentum:{c}" if c != "p" else "solve_pressure:p"
+        dofs = n ** 3 if c == "p" else (n - 1) * n * n
+        ms = per.get(key, 0.0)
+        solves[c] = {"ms_per_step": ms, "vcycles_per_step": cyc[c],
+                     "mdofs_per_vcycle": dofs * cyc[c] / (ms * 1e-3) / 1e6 if ms else None}
+    # dominant kernel: finest half-sweep of an edge-field (momentum) solve
+    eng = st.solvers["u"].engine(2, dev)
+    sweep_ms = eng.time_sweeps(0, 16)
+    edofs = (n - 1) * n * n
+    achieved = BYTES_PER_DOF_HALF_SWEEP * edofs / (sweep_ms * 1e-3) / 1e9
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        pass
+    # e2e: the same steps through the public API with host state: set_state
+    # from pinned host arrays, K steps, velocities and pressure back to host
+    hvel = {c: torch.zeros(tuple(st.velocity(c).interior.shape), dtype=torch.float64).pin_memory()
+            for c in st.comps}
+    hp = torch.zeros(tuple(st.pressure().interior.shape), dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    a.record(cur)
+    t2 = time.time()
+    st.set_state({c: hvel[c] for c in st.comps}, hp)
+    for _ in range(K):
+        st.step()
+    for c in st.comps:
+        hvel[c].copy_(st.velocity(c).interior, non_blocking=True)
+    hp.copy_(st.pressure().interior, non_blocking=True)
+    b.record(cur)
+    torch.cuda.synchronize()
+    clocks.mark(t2, time.time())
+    e2e_ms = a.elapsed_time(b) / K
+    state_bytes = (sum(v.numel() for v in hvel.values()) + hp.numel()) * 8
+    clocks.stop()
+    mem = torch.cuda.max_memory_allocated(dev)
+    line = {
+        "metric": NS_METRIC.format(n=n), "value": 1e3 / ms_step, "unit": "steps/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (cavity from rest)", "config": ns_config(n, world),
+        "solves": solves, "ms_per_step_by_formula": per,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_sweep_tma (finest edge-field u half-sweep)",
+                     "kernel_ms": sweep_ms, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": BYTES_PER_DOF_HALF_SWEEP * edofs},
+        "e2e": {"value": 1e3 / e2e_ms, "unit": "steps/s",
+                "h2d_bytes_per_step": state_bytes // K, "d2h_bytes_per_step": state_bytes // K,
+                "ms_per_step": e2e_ms,
+                "api": f"ProjectionStepper.set_state(host pinned) + {K} x step() + velocities "
+                       "and pressure to host; the state copies amortised over the steps"},
+        "cpu_baseline": None, "clocks": clocks.summary(),
+        "torch_max_allocated_gb": mem / 1e9,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = ns_cpu_sample(min(n, 256))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def ns_cpu_sample(m):
+    """One projection step of the pinned NS oracle (oracle/ns_oracle.py, C
+    kernels on all host threads) at m^3, after one warm-up step."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import ns_oracle as NO
+    threads = host_threads()
+    O.set_threads(threads)
+    orc = NO.NSOracle((m,) * 3, 100.0, 1e-3, 2, tol=1e-10, k_max=20, s=2,
+                      mesh_level=int(np.log2(m)) - 1)
+    orc.step()
+    t0 = time.perf_counter()
+    orc.step()
+    t = time.perf_counter() - t0
+    return {"value": 1.0 / t, "unit": "steps/s", "cores": threads, "kind": "port",
+            "sample": f"step 2 of the {m}^3 cavity by the oracle/ NS port (C kernels, OpenMP "
+                      f"{threads} threads); NOT the bench grid when m < n -- scale by (m/n)^3 "
+                      "for a rough per-DOF comparison", "grid": m}
+
+
+def ns_reference_arm(args):
+    n = ns_size(args)
+    K, W = args.steps, max(args.warmup, 3)
+    base = ns_cpu_sample(n)
+    line = {"impl": "reference", "metric": NS_METRIC.format(n=n), "value": base["value"],
+            "unit": "steps/s", "n_gpus": 1, "steps": 1, "warmup": 1,
+            "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (cavity from rest)",
+            "config": ns_config(n, 1), "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": f"requested K={K} W={W}; one timed step at this size (minutes of CPU)",
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def self_launch(args) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: relaunch this command under
+    torch.distributed.run with N processes (127.0.0.1 rendezvous) instead of
+    silently measuring one GPU."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] --gpus {args.gpus} without torchrun: relaunching as {' '.join(cmd)}",
+          file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.numba_child:
+        return numba_child(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        print(f"[bench] error: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return reference_arm(args)
+    if args.workload != "heat":
+        return ns_arm(args)
     return b200_arm(args)
 
 

@@ -80,6 +80,8 @@ struct NatView {
 struct AxisGeo {
     int m;       // cells along the axis (grid shape)
     int edge;    // 1 if the field is edge-centered along this axis
+    int iface = 0;  // slab interfaces (bit 0 lo, bit 1 hi): the rows beyond
+                    // hold a neighbour's data, not ghosts (fill_ghosts_slab)
 };
 
 // Is core index x along an axis "owned" (written) by that axis' pass?
@@ -87,6 +89,8 @@ struct AxisGeo {
 // m (always) and the low wall 0 unless periodic (never written, PKG/
 // boundary.py:117-125), plus rings beyond the walls.
 __device__ __forceinline__ bool owned(const AxisGeo& a, int lo_kind, int x) {
+    if ((a.iface & 1) && x <= 0) return false;
+    if ((a.iface & 2) && x >= (a.edge ? a.m : a.m + 1)) return false;
     if (!a.edge) return x <= 0 || x >= a.m + 1;
     if (x >= a.m) return true;
     if (x < 0) return true;

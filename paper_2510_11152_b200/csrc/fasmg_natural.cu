@@ -381,6 +381,8 @@ struct FillGeo {
     long slab_n[3]; // points per slab
     int lo[3][3];   // per slab a, per axis b: first data index
     int cnt[3][3];  // per slab a, per axis b: count
+    int olo[3];     // per axis: owned data indices 0..olo-1 on the low side
+    int fhi[3];     // per axis: first owned data index on the high side
 };
 
 struct DataReader {
@@ -406,18 +408,8 @@ __global__ void k_fill(double* data, FillGeo g, BcSpec bc) {
     // slab a enumerates the two owned ranges of axis a: cnt counts both
     // sides; map the linear index to the lo or hi side
     {
-        int c_lo = g.halo;  // owned lo indices along a (data 0..halo-1 or 0..halo-2)
-        const AxisGeo& A = g.ax[a];
-        int owned_lo = A.edge ? (bc.kind[a][0] == BC_PERIODIC ? g.halo - 1 : g.halo) : g.halo;
-        (void)c_lo;
-        int q = d[a] - g.lo[a][a];
-        int dat;
-        if (q < owned_lo) dat = q;  // data indices 0..owned_lo-1
-        else {
-            int first_hi = A.edge ? (g.halo - 1 + A.m) : (g.halo + A.m);
-            dat = first_hi + (q - owned_lo);
-        }
-        d[a] = dat;
+        const int q = d[a] - g.lo[a][a];
+        d[a] = q < g.olo[a] ? q : g.fhi[a] + (q - g.olo[a]);
     }
     // core index = data index - (halo - 1)
     int x[3] = {0, 0, 0};
@@ -975,9 +967,13 @@ int fasmg_weno_convect(double* out, const long* os, const double* const* vel, co
     return fasmg_check_launch();
 }
 
-// fill_ghosts on a natural-layout C-contiguous data array (PKG/boundary.py:90)
-int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, const int* kinds,
-                      const double* vals, void* stream) {
+// fill_ghosts on a natural-layout C-contiguous data array (PKG/boundary.py:90).
+// iface / ext0 serve the axis-0 slab form: interface sides of axis 0 are not
+// ghosts (the rows beyond hold a neighbour's data, exchanged beforehand) and
+// the local array has ext0 rows along axis 0.
+static int fill_ghosts_impl(double* data, int dim, const int* n, int ea, int halo,
+                            const int* kinds, const double* vals, int iface, int ext0,
+                            cudaStream_t stream) {
     if (dim != 2 && dim != 3) return fasmg_set_error(FASMG_EINVAL, "dim must be 2 or 3");
     FillGeo g;
     BcSpec bc;
@@ -990,21 +986,35 @@ int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, con
         }
         g.ax[a].m = a < dim ? n[a] : 1;
         g.ax[a].edge = (a == ea);
+        g.ax[a].iface = a == 0 ? iface : 0;
         g.ext[a] = a < dim ? (a == ea ? n[a] + 1 + 2 * (halo - 1) : n[a] + 2 * halo) : 1;
+        // owned data indices: low side 0..olo-1, high side fhi..fhi+ohi-1
+        const bool edge = (a == ea);
+        int olo = edge ? (bc.kind[a][0] == BC_PERIODIC ? halo - 1 : halo) : halo;
+        int ohi = halo;  // edge: wall m + rings; cell: halo rings
+        if (a == 0 && (iface & 1)) olo = 0;
+        if (a == 0 && (iface & 2)) ohi = 0;
+        g.olo[a] = olo;
+        g.fhi[a] = edge ? halo - 1 + g.ax[a].m : halo + g.ax[a].m;
+        g.cnt[a][a] = olo + ohi;  // refined below with lo
+        g.lo[a][a] = ohi;         // scratch: ohi until the slab loop
     }
+    if (ext0 > 0) g.ext[0] = ext0;
     if (dim == 2) { g.st[1] = 1; g.st[0] = g.ext[1]; g.st[2] = 0; }
     else { g.st[2] = 1; g.st[1] = g.ext[2]; g.st[0] = (long)g.ext[1] * g.ext[2]; }
+    int ohi[3];
+    for (int a = 0; a < 3; ++a) ohi[a] = g.lo[a][a];
     // slab a: owned along a; not owned along axes b < a; any along b > a.
     long maxn = 0;
     for (int a = 0; a < dim; ++a) {
         long cnt = 1;
         for (int b = 0; b < dim; ++b) {
             int c, lo;
-            const AxisGeo& B = g.ax[b];
-            int owned_lo = B.edge ? (bc.kind[b][0] == BC_PERIODIC ? halo - 1 : halo) : halo;
-            int owned_hi = B.edge ? halo : halo;  // edge: wall m + rings; cell: halo rings
-            if (b == a) { lo = 0; c = owned_lo + owned_hi; }
-            else if (b < a) { lo = owned_lo; c = g.ext[b] - owned_lo - owned_hi; }
+            if (b == a) { lo = 0; c = g.olo[b] + ohi[b]; }
+            else if (b < a) {  // up to the high owned rows, or the array end at an interface
+                lo = g.olo[b];
+                c = (ohi[b] ? g.fhi[b] : g.ext[b]) - g.olo[b];
+            }
             else { lo = 0; c = g.ext[b]; }
             g.lo[a][b] = lo;
             g.cnt[a][b] = c;
@@ -1015,9 +1025,28 @@ int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, con
     }
     if (maxn == 0) return 0;
     dim3 grid(nblk(maxn, TPB), dim);
-    if (dim == 2) k_fill<2><<<grid, TPB, 0, S(stream)>>>(data, g, bc);
-    else k_fill<3><<<grid, TPB, 0, S(stream)>>>(data, g, bc);
+    if (dim == 2) k_fill<2><<<grid, TPB, 0, stream>>>(data, g, bc);
+    else k_fill<3><<<grid, TPB, 0, stream>>>(data, g, bc);
     return fasmg_check_launch();
+}
+
+int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, const int* kinds,
+                      const double* vals, void* stream) {
+    return fill_ghosts_impl(data, dim, n, ea, halo, kinds, vals, 0, 0, S(stream));
+}
+
+// Axis-0 slab of a field: data is the rank's local
+// C-contiguous array with ext0 rows along axis 0, n[0] the rank's cells (an
+// edge field with edge axis 0 holds nodes 1..n[0] of the slab, n[0] being the
+// wall only on the last rank).  Sides flagged in iface (bit 0 lo, bit 1 hi)
+// are rank interfaces: their rows were filled from the neighbour (interior
+// values) and are only completed along axes 1..d-1, which is exactly what
+// the whole-field fill produces on those rows (every rule of axes >= 1 reads
+// its own row).
+int fasmg_fill_ghosts_slab(double* data, int dim, const int* n, int ea, int halo,
+                           const int* kinds, const double* vals, int iface, int ext0,
+                           void* stream) {
+    return fill_ghosts_impl(data, dim, n, ea, halo, kinds, vals, iface, ext0, S(stream));
 }
 
 // numpy's buffered-reduce chunk length for a C-order view of extent ext

@@ -23,12 +23,10 @@ def elem(op: int, out: torch.Tensor, inputs, s0: float = 0.0, s1: float = 0.0) -
     for t in ins:
         s = list(t.stride()) if t is not None else []
         st += s + [0] * (3 - len(s))
-    L = N.lib()
-    L.fasmg_ns_elem.restype = ctypes.c_int
     N.require_cuda(out)
-    N.check(L.fasmg_ns_elem(ctypes.c_int(op), N.ptr(out), N.strides(out), ptrs,
-                            (ctypes.c_long * 12)(*st), ctypes.c_double(s0), ctypes.c_double(s1),
-                            ctypes.c_int(out.dim()), N.ints(out.shape), N.torch_stream()))
+    N.call("fasmg_ns_elem", ctypes.c_int(op), N.ptr(out), N.strides(out), ptrs,
+           (ctypes.c_long * 12)(*st), ctypes.c_double(s0), ctypes.c_double(s1),
+           ctypes.c_int(out.dim()), N.ints(out.shape), N.torch_stream())
     return out
 
 
@@ -39,12 +37,9 @@ def laplacian(field, out: torch.Tensor | None = None) -> torch.Tensor:
     if out is None:
         out = torch.empty(shape, dtype=torch.float64, device=field.device)
     pc = field.core
-    L = N.lib()
-    L.fasmg_laplacian.restype = ctypes.c_int
-    N.check(L.fasmg_laplacian(N.ptr(out), N.strides(out), N.ptr(pc), N.strides(pc),
-                              ctypes.c_int(field.grid.dim), N.ints(shape),
-                              ctypes.c_double(1.0 / (field.grid.h * field.grid.h)),
-                              N.torch_stream()))
+    N.call("fasmg_laplacian", N.ptr(out), N.strides(out), N.ptr(pc), N.strides(pc),
+           ctypes.c_int(field.grid.dim), N.ints(shape),
+           ctypes.c_double(1.0 / (field.grid.h * field.grid.h)), N.torch_stream())
     return out
 
 

@@ -136,6 +136,9 @@ class ProjectionStepper:
         self._fp = Field(grid, Location.CELL, 1, device=self.device)
         self.held = {slot: q for q, slot in self.schedule.initial}  # slot -> quantity
         self.step_count = 0
+        # list to collect (formula, component, start event, end event) per
+        # executed Step on torch's current stream (bench.py), or None
+        self.timing = None
 
     # ------------------------------------------------------------ state I/O
     def resident_count(self) -> int:
@@ -233,7 +236,7 @@ class ProjectionStepper:
         rep = StepReport()
         scratch = {}
         sched = self.schedule
-        dt = self.params.dt
+        timing = self.timing
         for st in sched.steps:
             read = {}
             for q, slot in st.reads:
@@ -244,53 +247,65 @@ class ProjectionStepper:
                         raise MissingBinding(f"{st.describe()}: {q} not in {slot} "
                                              f"(holds {self.held.get(slot)})")
                     read[q] = self.slots[slot]
-            if st.formula == "rhs":
-                scratch[st.writes[0][1]] = self.momentum_rhs(st.comp, read)
-            elif st.formula in ("copy", "rotate2"):
-                moves = dict(st.copy_map)
-                for q, slot in st.writes:  # in order: the reference rotate2 semantics
-                    src = read[moves[q]]
-                    dst = self.slots[slot]
-                    if dst is not src:
-                        dst.data.copy_(src.data)
-                        dst.ghosts_fresh = src.ghosts_fresh
-                    self._bind(q, slot)
-            elif st.formula == "solve_momentum":
-                c = st.comp
-                q, slot = st.writes[0]
-                dst = self.slots[slot]
-                src = read[f"{c}_n"]
-                if dst is not src:
-                    dst.data.copy_(src.data)
-                rep.momentum[c] = self.solvers[c].solve(dst, read[f"f_{c}"], self.fas)
-                self._bind(q, slot)
-            elif st.formula == "solve_pressure":
-                q, slot = st.writes[0]
-                guess = self.slots[slot]
-                rep.pressure = self.pressure_poisson({c: read[f"{c}_tld"] for c in self.comps}, guess)
-                self._bind(q, slot)
-            elif st.formula == "correct":
-                c = st.comp
-                q, slot = st.writes[0]
-                dst = self.slots[slot]
-                # u^{n+1} = u~ - dt*(grad p~)_c, one pass
-                momentum_source(0, dst.interior, read[f"{c}_tld"], None, read["p_tld"],
-                                AXIS_OF[c], dt)
-                fill_ghosts(dst, self.bcs[c])
-                self._bind(q, slot)
-            elif st.formula == "p_update":
-                q, slot = st.writes[0]
-                dst = self.slots[slot]
-                elem(ADD, dst.interior, [read["p_n"].interior, read["p_tld"].interior])
-                dst.ghosts_fresh = False
-                self._bind(q, slot)
-            else:
-                raise ValueError(f"unknown formula {st.formula}")
+            if timing is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            self._exec(st, read, scratch, rep)
+            if timing is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                timing.append((st.formula, st.comp, e0, e1))
         ren = dict(sched.rebind)
         self.held = {slot: ren.get(q, q) for slot, q in self.held.items()}
         self.step_count += 1
-        self.t = self.step_count * dt
+        self.t = self.step_count * self.params.dt
         return rep
+
+    def _exec(self, st, read: dict, scratch: dict, rep: StepReport):
+        """Execute one schedule Step on device fields."""
+        dt = self.params.dt
+        if st.formula == "rhs":
+            scratch[st.writes[0][1]] = self.momentum_rhs(st.comp, read)
+        elif st.formula in ("copy", "rotate2"):
+            moves = dict(st.copy_map)
+            for q, slot in st.writes:  # in order: the reference rotate2 semantics
+                src = read[moves[q]]
+                dst = self.slots[slot]
+                if dst is not src:
+                    dst.data.copy_(src.data)
+                    dst.ghosts_fresh = src.ghosts_fresh
+                self._bind(q, slot)
+        elif st.formula == "solve_momentum":
+            c = st.comp
+            q, slot = st.writes[0]
+            dst = self.slots[slot]
+            src = read[f"{c}_n"]
+            if dst is not src:
+                dst.data.copy_(src.data)
+            rep.momentum[c] = self.solvers[c].solve(dst, read[f"f_{c}"], self.fas)
+            self._bind(q, slot)
+        elif st.formula == "solve_pressure":
+            q, slot = st.writes[0]
+            guess = self.slots[slot]
+            rep.pressure = self.pressure_poisson({c: read[f"{c}_tld"] for c in self.comps}, guess)
+            self._bind(q, slot)
+        elif st.formula == "correct":
+            c = st.comp
+            q, slot = st.writes[0]
+            dst = self.slots[slot]
+            # u^{n+1} = u~ - dt*(grad p~)_c, one pass
+            momentum_source(0, dst.interior, read[f"{c}_tld"], None, read["p_tld"],
+                            AXIS_OF[c], dt)
+            fill_ghosts(dst, self.bcs[c])
+            self._bind(q, slot)
+        elif st.formula == "p_update":
+            q, slot = st.writes[0]
+            dst = self.slots[slot]
+            elem(ADD, dst.interior, [read["p_n"].interior, read["p_tld"].interior])
+            dst.ghosts_fresh = False
+            self._bind(q, slot)
+        else:
+            raise ValueError(f"unknown formula {st.formula}")
 
     def _bind(self, q: str, slot: str):
         self.held[slot] = q
