@@ -115,6 +115,14 @@ int fasmg_weno_deriv0_3d(double* out, const long* os, const double* q, const lon
  * of a field with n[dim] cells, edge axis ea and halo `halo` */
 int fasmg_fill_ghosts(double* data, int dim, const int* n, int ea, int halo, const int* kinds,
                       const double* vals, void* stream);
+/* the same fill on one rank's axis-0 slab of a field (local C-contiguous
+ * array with ext0 rows along axis 0, n[0] the slab's cells): sides flagged
+ * in iface (bit 0 lo, bit 1 hi) are rank interfaces whose rows hold the
+ * neighbour's interior values; they are completed along axes 1..d-1 only,
+ * the boundary condition applies on global walls (ns_slab.py) */
+int fasmg_fill_ghosts_slab(double* data, int dim, const int* n, int ea, int halo,
+                           const int* kinds, const double* vals, int iface, int ext0,
+                           void* stream);
 /* np.sum of a (non-contiguous) interior view in numpy 2.3's buffered-reduce
  * order, used by the mean projection (PKG/fas.py:145,156); out[0] on device.
  * scratch >= prod(ext) doubles; sums >= fasmg_view_sum_chunks() doubles */

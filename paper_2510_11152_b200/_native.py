@@ -47,6 +47,7 @@ _SIGS = {
     "fasmg_weno_deriv0_2d": "pspsps" + "iiii" + "dd" + "S",
     "fasmg_weno_deriv0_3d": "pspsps" + "iiiiii" + "dd" + "S",
     "fasmg_fill_ghosts": "piIiiIDS",
+    "fasmg_fill_ghosts_slab": "piIiiIDiiS",
     "fasmg_view_sum": "psiIpppS",
     "fasmg_view_sumsq": "psiIppS",
     "fasmg_sub_mean": "psiIpdS",

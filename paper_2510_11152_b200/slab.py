@@ -223,6 +223,65 @@ class VirtualSlabSolver:
         p.ghosts_fresh = False
         return p
 
+    def _views_interior(self, v: torch.Tensor, halo: int, rank: int) -> torch.Tensor:
+        g = self.hierarchy.fine
+        ea = self.location.edge_axis
+        m0 = g.shape[0] // self.parts
+        if ea == 0 and rank == self.parts - 1:
+            m0 -= 1  # the wall node n
+        sl = [slice(1, 1 + m0)]
+        for a in range(1, g.dim):
+            sl.append(slice(halo, halo + (g.shape[a] - 1 if a == ea else g.shape[a])))
+        return v[tuple(sl)]
+
+    def _views_subtract_mean(self, vs, halo: int):
+        """``interior -= np.mean(interior)`` over a field held as per-rank
+        slab views: chunk sums per slab, totalled in rank/chunk order
+        (bitwise numpy's order, as dist_subtract_interior_mean)."""
+        g = self.hierarchy.fine
+        ea = self.location.edge_axis
+        gext = tuple(g.shape[a] - 1 if a == ea else g.shape[a] for a in range(g.dim))
+        ivs = [self._views_interior(v, halo, r) for r, v in enumerate(vs)]
+        total = ordered_total([slab_chunk_sums(v, gext).cpu() for v in ivs])
+        tot = torch.tensor([total], dtype=torch.float64, device=vs[0].device)
+        for v in ivs:
+            N.call("fasmg_sub_mean", N.ptr(v), N.strides(v), v.dim(), N.ints(v.shape),
+                   N.ptr(tot), float(math.prod(gext)), N.torch_stream())
+
+    def solve_views(self, pvs, fvs, params: FasParams, halo_p: int = 1,
+                    halo_f: int = 1) -> SolveReport:
+        """``solve`` on per-rank slab views (rank cells + 1 ghost plane each
+        side along axis 0, as DistSlabSolver.solve takes them): the
+        virtual-rank form of the distributed solve, singular mean included.
+        Ghost values of the views are left to the caller."""
+        singular = self._singular()
+        if singular:
+            self._views_subtract_mean(fvs, halo_f)
+        es = self.engines(params.s, pvs[0].device)
+        for e, pv, fv in zip(es, pvs, fvs):
+            e.load(pv, fv, halo_p, halo_f)
+        for e in es:
+            e.synchronize()
+        for e in es:
+            e.sync_halos()
+        g = self.hierarchy.fine
+        scale = g.h ** (g.dim / 2.0)
+        history = []
+        for _ in range(params.k_max):
+            self.launch_all(es, 1, True)
+            sums = [e.result() for e in es]
+            if any(x != sums[0] for x in sums):
+                raise NativeError(f"ranks disagree on the residual: {sums}")
+            res = scale * math.sqrt(sums[0])
+            history.append(res)
+            if res <= params.tol:
+                break
+        for e, pv in zip(es, pvs):
+            e.store(pv, halo_p)
+        if singular:
+            self._views_subtract_mean(pvs, halo_p)
+        return SolveReport(len(history), history, bool(history and history[-1] <= params.tol))
+
     def solve(self, p: Field, f: Field, params: FasParams) -> SolveReport:
         singular = self._singular()
         if singular:
