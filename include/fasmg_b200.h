@@ -212,11 +212,6 @@ long fasmg_engine_kernels_per_vcycle(void* engine, int with_norm);
  * half-sweep launch on `level`, over `reps` launches */
 int fasmg_engine_time_sweeps(void* engine, int level, int reps, double* ms);
 int fasmg_engine_level_info(void* engine, int level, long* info);
-/* debug: run level `level`'s first wavefront smoothing launch with a trace
- * of 6 globaltimer stamps per work item (poll start, deps met, TMA issued,
- * data landed, computed, published) copied into host `out` (capacity `cap`
- * stamps); *n = item count */
-int fasmg_engine_wave_trace(void* engine, int level, unsigned long long* out, long cap, long* n);
 
 /* ---- axis-0 slab decomposition -------------------
  * One engine per rank owns the slab `rank` of every level whose block-plane
@@ -242,6 +237,10 @@ int fasmg_engine_slab_info(void* engine, int* out);
 int fasmg_engine_sync_halos(void* engine);
 /* asynchronous run/result pair (ranks that must run concurrently) */
 int fasmg_engine_launch(void* engine, int count, int with_norm);
+/* capture + instantiate the V-cycle graph without launching it; every rank
+ * sharing a device is prepared before any launches (lazy module loading
+ * would otherwise wait on the peers' spin-waits) */
+int fasmg_engine_prepare(void* engine, int with_norm);
 int fasmg_engine_result(void* engine, double* sumsq);
 /* test access: level geometry [cls, s0, s1, E0, E1, E2, B0, off0, G0] and a
  * device copy of a level's blocked P (which=0) or F (which=1) arrays */

@@ -102,7 +102,6 @@ __device__ __forceinline__ bool interior(const Lvl& L, int c, const int* bb) {
 #include "fasmg_stencil.cuh"
 #include "fasmg_wave.cuh"
 #include "fasmg_coarse.cuh"
-#include "fasmg_fused.cuh"
 
 // ------------------------------------------------- edge-centered transfers
 // Reader of raw stored values at GLOBAL core (grid) index x in the blocked
@@ -850,16 +849,8 @@ struct Engine {
     Arena* arena = nullptr;             // shared level arrays (nullptr: private)
     std::vector<void*> owned;           // level arrays this engine frees
     bool sharded(int k) const { return nranks > 1 && k < kg; }
-    // ---- temporally blocked smoothing (fasmg_wave.cuh) ----
-    int wave_T = 0;                     // FASMG_WAVE_T: half-sweeps per launch (0: off)
-    int wave_lag = 2;                   // FASMG_WAVE_LAG: ticket-order lag (1 or 2)
-    int wave_K = 4;                     // FASMG_WAVE_K: tiles per ticket
-    long wave_min = 1L << 18;           // FASMG_WAVE_MIN: min interior blocks of a level
-    int wave_grid = 0;                  // resident CTAs (occupancy x SMs)
-    unsigned* wave_buf = nullptr;       // ticket + [T][B0+2] completion counters
-    bool wave_ok[32] = {};
     bool tma_ok[32] = {};               // level k half-sweeps use k_sweep_tma
-    CUtensorMap mapH[32], mapI[32], mapF[32], mapT[32], mapP8[32];
+    CUtensorMap mapF[32], mapT[32];
     int resid_tma = 1;                  // FASMG_RESID_TMA: tau / norm on the TMA march
     int corr_fuse = 1;                  // FASMG_CORR_FUSE: correction fused into the first post half-sweep
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
@@ -869,12 +860,6 @@ struct Engine {
     int coarse_cs = 8;                  // FASMG_COARSE_CS: CTAs per cluster
     long coarse_max = 4096;             // FASMG_COARSE_MAX: max blocks of a coarse level
     CoarseArgs* dcoarse = nullptr;      // device copy of the level table
-    // ---- last half-sweep fused with the residual (fasmg_fused.cuh) ----
-    int fuse = 0;                       // FASMG_FUSE bits: 1 tau pass, 2 outer norm (measured slower: off)
-    bool fuse_ok[32] = {};
-    CUtensorMap mapR[32], mapG[32];     // P boxes 36x12, F boxes 36x10
-    int npart_fused = 0;                // partial sums written by the fused norm
-    double* dbg = nullptr;              // FASMG_FUSE_DEBUG: per-point fused residual (level 0)
 };
 
 struct Tile {
@@ -908,8 +893,8 @@ static bool resid_tma_level(const Engine& E, int k) {
 // (k_sweep_tma<.., CORR>): 3D cell-centred TMA level, unsharded, no periodic
 // face, first two half-sweeps complementary X/RBGS color groups
 static bool corr_fused(const Engine& E, int k) {
-    if (!E.corr_fuse || E.fuse || E.dim != 3 || E.ea >= 0 || !E.tma_ok[k] || E.sharded(k) ||
-        k + 1 >= E.nl || !E.PI[k + 1] || E.masks.size() < 2 || E.wave_T > 0)
+    if (!E.corr_fuse || E.dim != 3 || E.ea >= 0 || !E.tma_ok[k] || E.sharded(k) ||
+        k + 1 >= E.nl || !E.PI[k + 1] || E.masks.size() < 2)
         return false;
     for (int a = 0; a < 3; ++a)
         if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
@@ -1230,49 +1215,6 @@ static void gather_level(Engine& E, int k, long& cnt) {
     launch_pad_fill<D>(E, k, cnt);
 }
 
-// T half-sweeps (seq[i0 .. i0+T)) of level k in one wavefront launch
-static void launch_wave(Engine& E, int k, const std::vector<unsigned>& seq, int i0, int T,
-                        long& cnt, unsigned long long* trace = nullptr) {
-    const Lvl& L = E.L[k];
-    WaveArgs A;
-    A.P = E.P[k];
-    A.T = T;
-    A.odd = 0;
-    for (int t = 0; t < T; ++t)
-        if (seq[i0 + t] == 0x96u) A.odd |= 1u << t;
-    A.ntx = L.B[2] / wave::TX;
-    A.nty = L.B[1] / wave::TY;
-    A.K = std::max(1, E.wave_K);
-    A.K = std::min(A.K, A.ntx);
-    A.gpr = (A.ntx + A.K - 1) / A.K;
-    A.ng = A.gpr * A.nty;
-    A.ticket = E.wave_buf;
-    A.flags = E.wave_buf + 32;  // keep the hot ticket on its own line
-    A.lag = E.wave_lag;
-    A.cyc1 = E.bc.kind[1][0] == BC_PERIODIC ? 1 : 0;
-    A.trace = trace;
-    A.ngroups = (long long)(L.B[0] + A.lag * (T - 1)) * T * A.ng;
-    cudaMemsetAsync(E.wave_buf, 0, sizeof(unsigned) * (32 + (size_t)T * (L.B[0] + 2) * A.nty),
-                    E.stream);
-    const int grid = (int)std::min<long long>(E.wave_grid, A.ngroups);
-    EA_DISPATCH(3, E.ea, (k_smooth_wave<EA><<<grid, wave::NTHR, wave::SMEM, E.stream>>>(
-                             E.mapH[k], E.mapI[k], E.mapF[k], L, E.bc, A)));
-    ++cnt;
-}
-
-// can the smoothing sequence of level k run as wavefront launches?
-static bool wave_seq(const Engine& E, int k, std::vector<unsigned>& seq) {
-    if (!E.wave_ok[k] || E.wave_T <= 0) return false;
-    seq.clear();
-    for (int it = 0; it < E.s; ++it)
-        for (unsigned m : E.masks) {
-            if (m != 0x96u && m != 0x69u) return false;
-            seq.push_back(m);
-        }
-    return true;
-}
-
-// skip_last: leave the stage's final half-sweep to a fused kernel
 // the first post-smoothing half-sweep of level k with the coarse correction
 // applied on the fly (k_sweep_tma<-1, M, true>; see corr_fused)
 static void launch_sweep_corr(Engine& E, int k, unsigned m) {
@@ -1291,22 +1233,12 @@ static void launch_sweep_corr(Engine& E, int k, unsigned m) {
 }
 
 template <int D>
-static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false,
-                          bool first_corr = false) {
-    std::vector<unsigned> seq;
-    if (D == 3 && !first_corr && wave_seq(E, k, seq)) {
-        const int n = (int)seq.size() - (skip_last ? 1 : 0);
-        for (int i = 0; i < n; i += E.wave_T) launch_wave(E, k, seq, i, std::min(E.wave_T, n - i), cnt);
-        return;
-    }
+static void launch_smooth(Engine& E, int k, long& cnt, bool first_corr = false) {
     const Tile t = tile_of(E.L[k]);
-    const int total = E.s * (int)E.masks.size();
-    int done = 0;
     for (int it = 0; it < E.s; ++it)
         for (unsigned m : E.masks) {
-            if (skip_last && ++done == total) return;
             bool pushed = false;
-            if (first_corr && it == 0 && m == E.masks[0] && done <= 1) {
+            if (first_corr && it == 0 && m == E.masks[0]) {
                 launch_sweep_corr(E, k, m);
                 first_corr = false;
             } else {
@@ -1315,46 +1247,6 @@ static void launch_smooth(Engine& E, int k, long& cnt, bool skip_last = false,
             ++cnt;
             halo_exchange<D>(E, k, m, cnt, pushed);
         }
-}
-
-// can level k's last smoothing half-sweep run fused with the residual?
-static bool fused_level(const Engine& E, int k, int mode_bit = 1) {
-    if (!(E.fuse & mode_bit) || !E.fuse_ok[k] || E.masks.empty()) return false;
-    const unsigned m = E.masks.back();
-    return m == 0x96u || m == 0x69u;
-}
-
-static dim3 fused_grid(const Lvl& L, int* chunk_out, int march_chunk) {
-    using namespace fsw;
-    const long tiles = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
-    int chunk = march_chunk;
-    if (chunk <= 0) {
-        chunk = 4;
-        for (int c = 16; c >= 8; c >>= 1)
-            if (tiles * ((L.B[0] + c - 1) / c) >= 592) { chunk = c; break; }
-    }
-    *chunk_out = chunk;
-    return dim3((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
-}
-
-template <int MODE>
-static void launch_fused(Engine& E, int k, long& cnt) {
-    const Lvl& L = E.L[k];
-    const Lvl& Lc = MODE == fsw::MODE_TAU ? E.L[k + 1] : L;
-    double* Pc = MODE == fsw::MODE_TAU ? E.P[k + 1] : nullptr;
-    double* Fc = MODE == fsw::MODE_TAU ? E.F[k + 1] : E.dbg;
-    int chunk = 0;
-    const dim3 grd = fused_grid(L, &chunk, E.march_chunk);
-    const dim3 blk(fsw::TX, fsw::TY, 1);
-    const Lvl& Ld = L;
-    if (E.masks.back() == 0x96u)
-        k_sweep_resid<MODE, 0x96u><<<grd, blk, fsw::SMEM, E.stream>>>(
-            E.mapR[k], E.mapG[k], E.mapF[k], E.P[k], Ld, E.bc, chunk, E.part, Pc, Fc, Lc);
-    else
-        k_sweep_resid<MODE, 0x69u><<<grd, blk, fsw::SMEM, E.stream>>>(
-            E.mapR[k], E.mapG[k], E.mapF[k], E.P[k], Ld, E.bc, chunk, E.part, Pc, Fc, Lc);
-    ++cnt;
-    launch_pad_fill<3>(E, k, cnt);  // the deferred ghost pads of the new B values
 }
 
 template <int D>
@@ -1374,10 +1266,8 @@ static void launch_coarse(Engine& E, long& cnt) {
     ++cnt;
 }
 
-// fuse_norm: the finest level's last half-sweep also produces the outer
-// residual's partial sums (launch_norm then only reduces them)
 template <int D>
-static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
+static void launch_vcycle(Engine& E, long& cnt) {
     const unsigned ALL = (1u << (1 << D)) - 1;
     // levels >= kc run inside one cluster launch
     const int kc = E.coarse_k0 >= 0 ? E.coarse_k0 : E.nl;
@@ -1390,14 +1280,9 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L), tc = tile_of(Lc);
-        if (D == 3 && fused_level(E, k)) {
-            launch_smooth<D>(E, k, cnt, true);
-            launch_fused<fsw::MODE_TAU>(E, k, cnt);
-        } else {
-            launch_smooth<D>(E, k, cnt);
-        }
+        launch_smooth<D>(E, k, cnt);
         if (E.ea < 0) {
-            if (!(D == 3 && fused_level(E, k))) {
+            {
                 if (D == 3 && resid_tma_level(E, k)) {
                     const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
                     k_resid_tma<1><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
@@ -1482,26 +1367,16 @@ static void launch_vcycle(Engine& E, long& cnt, bool fuse_norm = false) {
             launch_pad_fill<D>(E, k, cnt);
         }
         halo_exchange<D>(E, k, ALL, cnt);
-        if (k == 0 && fuse_norm) {
-            launch_smooth<D>(E, k, cnt, true, cf);
-            launch_fused<fsw::MODE_NORM>(E, k, cnt);
-        } else {
-            launch_smooth<D>(E, k, cnt, false, cf);
-        }
+        launch_smooth<D>(E, k, cnt, cf);
     }
 }
 
 template <int D>
-static bool norm_fusable(const Engine& E) {
-    return D == 3 && E.nl > 1 && E.coarse_k0 != 0 && fused_level(E, 0, 2);
-}
-
-template <int D>
-static void launch_norm(Engine& E, long& cnt, bool fused = false) {
+static void launch_norm(Engine& E, long& cnt) {
     const Lvl& L = E.L[0];
     const Tile t = tile_of(L);
     int npart_norm = E.npart;
-    if (!fused) {
+    {
         if (D == 3 && E.resid_tma && E.tma_ok[0] && !E.sharded(0)) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
@@ -1523,7 +1398,7 @@ static void launch_norm(Engine& E, long& cnt, bool fused = false) {
                                      E.P[0], E.F[0], L, E.part)));
         ++cnt;
     }
-    k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, fused ? E.npart_fused : npart_norm, E.dsum);
+    k_final_sum<<<1, 1024, 0, E.stream>>>(E.part, npart_norm, E.dsum);
     ++cnt;
     if (E.nranks > 1) {  // fixed rank-order sum of the partials on every rank
         const int P = E.nranks, r = E.rank;
@@ -1550,9 +1425,8 @@ static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* e
     cudaError_t e = cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return fasmg_check(e);
     if (E.dim == 3) {
-        const bool fz = with_norm && norm_fusable<3>(E);
-        launch_vcycle<3>(E, cnt, fz);
-        if (with_norm) launch_norm<3>(E, cnt, fz);
+        launch_vcycle<3>(E, cnt);
+        if (with_norm) launch_norm<3>(E, cnt);
     } else {
         launch_vcycle<2>(E, cnt);
         if (with_norm) launch_norm<2>(E, cnt);
@@ -1610,16 +1484,6 @@ static bool encode_map2d(CUtensorMap* m, double* base, const Lvl& L, unsigned bx
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Decide which levels smooth by wavefront launches and prepare them.
-template <int EA>
-static int wave_attr(int* occ) {
-    cudaError_t e = cudaFuncSetAttribute(k_smooth_wave<EA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)wave::SMEM);
-    if (e != cudaSuccess) return fasmg_check(e);
-    return fasmg_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_smooth_wave<EA>,
-                                                                     wave::NTHR, wave::SMEM));
-}
-
 template <int EA>
 static int tma_attr() {
     const int sm = (int)tsw::SMEM;
@@ -1673,8 +1537,7 @@ static int tma_setup(Engine& E) {
         const Lvl& L = E.L[k];
         if (L.B[2] < 32 || L.B[1] < 8 || L.nblk < min_blocks) continue;
         E.tma_ok[k] = encode_map(&E.mapT[k], E.P[k], L, tsw::HX, tsw::HY) &&
-                      encode_map(&E.mapF[k], E.F[k], L, tsw::TX, tsw::TY) &&
-                      encode_map(&E.mapP8[k], E.P[k], L, tsw::TX, tsw::TY);
+                      encode_map(&E.mapF[k], E.F[k], L, tsw::TX, tsw::TY);
         any = any || E.tma_ok[k];
     }
     if (!any) return 0;
@@ -1743,81 +1606,6 @@ static int coarse_setup(Engine& E) {
     }
     if (!st) E.coarse_k0 = k0;
     return st;
-}
-
-template <int MODE>
-static int fused_attr() {
-    const int sm = (int)fsw::SMEM;
-    cudaError_t e = cudaFuncSetAttribute(k_sweep_resid<MODE, 0x96u>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_sweep_resid<MODE, 0x69u>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    return fasmg_check(e);
-}
-
-// levels whose last half-sweep fuses with the residual: 3D cell-centred,
-// unsharded TMA levels, no periodic face (FASMG_FUSE=0 disables)
-static int fused_setup(Engine& E) {
-    if (const char* v = getenv("FASMG_FUSE")) E.fuse = atoi(v);
-    if (!E.fuse || E.dim != 3 || E.ea >= 0) return 0;
-    for (int a = 0; a < 3; ++a)
-        if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return 0;
-    bool any = false;
-    for (int k = 0; k < E.nl - 1; ++k) {
-        if (!E.tma_ok[k] || E.sharded(k)) continue;
-        const Lvl& L = E.L[k];
-        E.fuse_ok[k] = encode_map(&E.mapR[k], E.P[k], L, fsw::AX, fsw::AY) &&
-                       encode_map(&E.mapG[k], E.F[k], L, fsw::FX, fsw::FY);
-        any = any || E.fuse_ok[k];
-    }
-    if (!any) return 0;
-    int st = fused_attr<fsw::MODE_NORM>();
-    if (!st) st = fused_attr<fsw::MODE_TAU>();
-    if (st) return st;
-    if (getenv("FASMG_FUSE_DEBUG")) {
-        size_t bytes = sizeof(double) * (size_t)E.L[0].cls * 8;
-        if (int st = fasmg_check(cudaMalloc(&E.dbg, bytes))) return st;
-        cudaMemsetAsync(E.dbg, 0, bytes, E.stream);
-    }
-    if (E.fuse_ok[0]) {
-        int chunk = 0;
-        const dim3 g = fused_grid(E.L[0], &chunk, E.march_chunk);
-        E.npart_fused = (int)(g.x * g.y * g.z);
-        if (E.npart_fused > E.npart) return fasmg_set_error(FASMG_EINVAL, "fused norm partials exceed buffer");
-    }
-    return 0;
-}
-
-static int wave_setup(Engine& E) {
-    if (int st = coarse_setup(E)) return st;
-    if (int st = tma_setup(E)) return st;
-    if (const char* v = getenv("FASMG_WAVE_T")) E.wave_T = std::max(0, std::min(32, atoi(v)));
-    if (const char* v = getenv("FASMG_WAVE_K")) E.wave_K = std::max(1, atoi(v));
-    if (const char* v = getenv("FASMG_WAVE_LAG")) E.wave_lag = std::max(1, std::min(4, atoi(v)));
-    if (const char* v = getenv("FASMG_WAVE_MIN")) E.wave_min = atol(v);
-    if (E.dim != 3 || E.wave_T <= 0 || E.sweep_variant < 3) return 0;
-    if (E.bc.kind[0][0] == BC_PERIODIC || E.bc.kind[0][1] == BC_PERIODIC) return 0;
-    long maxp = 0;
-    for (int k = 0; k < E.nl; ++k) {
-        const Lvl& L = E.L[k];
-        if (E.sharded(k) || L.nblk < E.wave_min || L.B[2] % wave::TX || L.B[1] % wave::TY) continue;
-        E.wave_ok[k] = encode_map(&E.mapH[k], E.P[k], L, wave::HX, wave::HY) &&
-                       encode_map(&E.mapI[k], E.P[k], L, wave::TX, wave::TY) &&
-                       encode_map(&E.mapF[k], E.F[k], L, wave::TX, wave::TY);
-        if (E.wave_ok[k]) maxp = std::max(maxp, ((long)L.B[0] + 2) * (L.B[1] / wave::TY));
-    }
-    if (!maxp) return 0;
-    int occ = 0, dev = 0, sms = 0;
-    int st = 0;
-    EA_DISPATCH(3, E.ea, (st = wave_attr<EA>(&occ)));
-    if (st) return st;
-    if ((st = fasmg_check(cudaGetDevice(&dev)))) return st;
-    if ((st = fasmg_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)))) return st;
-    E.wave_grid = std::max(1, occ) * sms;
-    const size_t bytes = sizeof(unsigned) * (32 + (size_t)E.wave_T * maxp);
-    if ((st = fasmg_check(cudaMalloc(&E.wave_buf, bytes)))) return st;
-    return fasmg_check(cudaMemsetAsync(E.wave_buf, 0, bytes, E.stream));
 }
 
 static Lvl make_lvl(int dim, const int* n, int ea, double dmin, double dmax, double a,
@@ -1980,8 +1768,8 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
         for (int t = 0; t < dim; ++t) nn[t] /= 2;
     }
     E->npart = (int)tile_ctas(tile_of(E->L[0]));
-    if (int st = wave_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (TMA maps, coarse cluster, wavefront) failed"); return nullptr; }
-    if (int st = fused_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (fused residual) failed"); return nullptr; }
+    if (int st = coarse_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (coarse cluster) failed"); return nullptr; }
+    if (int st = tma_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (TMA maps) failed"); return nullptr; }
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
         fasmg_check(cudaMallocHost(&E->hsum, sizeof(double))) ||
@@ -2126,7 +1914,6 @@ void fasmg_engine_destroy(void* h) {
     cudaFree(E->flags);
     cudaFree(E->cnt);
     cudaFree(E->allpart);
-    if (E->wave_buf) cudaFree(E->wave_buf);
     if (E->dcoarse) cudaFree(E->dcoarse);
     delete E;
 }
@@ -2202,9 +1989,8 @@ int fasmg_engine_run(void* h, int count, int with_norm, double* sumsq, int use_g
         } else {
             long cnt = 0;
             if (E->dim == 3) {
-                const bool fz = with_norm && norm_fusable<3>(*E);
-                launch_vcycle<3>(*E, cnt, fz);
-                if (with_norm) launch_norm<3>(*E, cnt, fz);
+                launch_vcycle<3>(*E, cnt);
+                if (with_norm) launch_norm<3>(*E, cnt);
             } else {
                 launch_vcycle<2>(*E, cnt);
                 if (with_norm) launch_norm<2>(*E, cnt);
@@ -2237,6 +2023,21 @@ int fasmg_engine_launch(void* h, int count, int with_norm) {
     return 0;
 }
 
+// Capture and instantiate the V-cycle graph (with_norm selects the variant)
+// without launching it.  Ranks that share a device must all be prepared
+// before any of them launches: capturing a kernel for the first time loads
+// its module lazily (CUDA_MODULE_LOADING=LAZY, the default), and a lazy
+// load waits for the device's running kernels -- which include the peers'
+// k_wait spins on this rank, so launching one rank while another is still
+// capturing deadlocks until k_wait's guard traps.
+int fasmg_engine_prepare(void* h, int with_norm) {
+    Engine* E = (Engine*)h;
+    cudaGraphExec_t* ex = with_norm ? &E->exec_vn : &E->exec_v;
+    cudaGraph_t* g = with_norm ? &E->graph_vn : &E->graph_v;
+    if (!*ex) return capture(*E, with_norm != 0, g, ex);
+    return 0;
+}
+
 int fasmg_engine_result(void* h, double* sumsq) {
     Engine* E = (Engine*)h;
     int st = fasmg_check(cudaStreamSynchronize(E->stream));
@@ -2258,7 +2059,7 @@ int fasmg_engine_level_geom(void* h, int k, long* out) {
 int fasmg_engine_level_copy(void* h, int k, int which, double* dst) {
     Engine* E = (Engine*)h;
     if (k < 0 || k >= E->nl) return fasmg_set_error(FASMG_EINVAL, "level out of range");
-    const double* src = which == 0 ? E->P[k] : (which == 1 ? E->F[k] : E->dbg);
+    const double* src = which == 0 ? E->P[k] : (which == 1 ? E->F[k] : nullptr);
     if (!src) return fasmg_set_error(FASMG_EINVAL, "no such array");
     int st = fasmg_check(cudaStreamSynchronize(E->stream));
     if (st) return st;
@@ -2304,32 +2105,6 @@ int fasmg_engine_time_sweeps(void* h, int k, int reps, double* ms) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     return st ? st : fasmg_check_launch();
-}
-
-// Debug: run the first wavefront launch of level k's smoothing stage with a
-// trace buffer of 6 globaltimer stamps per item (t, b0, tile) and copy it to
-// host memory `out` (size 6*T*B0*ntiles).  Returns the item count in *n.
-int fasmg_engine_wave_trace(void* h, int k, unsigned long long* out, long cap, long* n) {
-    Engine* E = (Engine*)h;
-    std::vector<unsigned> seq;
-    if (E->dim != 3 || k < 0 || k >= E->nl || !wave_seq(*E, k, seq))
-        return fasmg_set_error(FASMG_EINVAL, "level does not use wavefront smoothing");
-    const Lvl& L = E->L[k];
-    const int T = std::min(E->wave_T, (int)seq.size());
-    const long items = (long)T * L.B[0] * (L.B[2] / wave::TX) * (L.B[1] / wave::TY);
-    *n = items;
-    if (cap < 6 * items) return fasmg_set_error(FASMG_EINVAL, "trace buffer too small");
-    unsigned long long* d = nullptr;
-    int st = fasmg_check(cudaMalloc(&d, sizeof(unsigned long long) * 6 * items));
-    if (st) return st;
-    cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 6 * items, E->stream);
-    long cnt = 0;
-    launch_wave(*E, k, seq, 0, T, cnt, d);
-    st = fasmg_check(cudaMemcpyAsync(out, d, sizeof(unsigned long long) * 6 * items,
-                                     cudaMemcpyDeviceToHost, E->stream));
-    if (!st) st = fasmg_check(cudaStreamSynchronize(E->stream));
-    cudaFree(d);
-    return st;
 }
 
 // kernels launched per V-cycle (with_norm: V-cycle + outer residual norm),

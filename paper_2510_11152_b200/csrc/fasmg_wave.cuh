@@ -1,56 +1,12 @@
-// fasmg_wave.cuh -- temporally blocked X-MCGS smoothing for large 3D levels
-// (included by fasmg_engine.cu inside namespace fasmg, after
-// fasmg_stencil.cuh).
-//
-// One persistent launch runs T consecutive half-sweeps of one level (the 8
-// half-sweeps of a smoothing stage at s=2, 'ff': PKG/fas.py:98,124 calling
-// PKG/smoothers.py:136-153 twice) as a wavefront along block axis 0.
-//
-// Work item = (half-sweep t, block plane b0, 32x8 tile of (b2, b1) blocks).
-// A half-sweep's 7-point stencil reaches one block either side along every
-// axis, so item (t, b, tile in tile row r) may run once half-sweep t-1 has
-// finished tile rows r-1..r+1 of planes b-1..b+1 (its inputs are final, and
-// every earlier reader of the classes it overwrites is done -- transitively
-// this covers all earlier half-sweeps).  A tile row spans the whole b2
-// extent, which covers the in-plane periodic wrap along b2; with a periodic
-// b1 axis the first and last tile rows are neighbours (the b1 ghost row of
-// one is written by the other).  A periodic axis 0 would couple the first
-// and last planes and is not run by this kernel.
-//
-// Every point is updated with exactly the arithmetic and the ghost-pad
-// maintenance of k_sweep_smem / k_sweep_fast, and in the same dependency
-// order as the reference's color sequence, so results are bitwise equal.
-//
-// CTA = 8 consumer warps (one thread per block of the tile; the 4 classes
-// of the half-sweep's color) + 1 producer warp + 1 signaler warp.  The producer takes
-// tickets, waits for the item's dependency counters (ld.acquire.gpu), and
-// issues TMA box loads into a 4-stage shared-memory ring (mbarrier
-// complete_tx): per item the 4 opposite-parity classes at plane b0 with the
-// in-plane halo the stencil needs (36 x 9: a TMA box must start on a 16-byte
-// boundary -- an odd fp64 start coordinate is an illegal instruction on
-// B200 -- so the column halo is widened to x0-2..x0+33), each opposite class's one
-// axis-0 neighbor plane (32 x 8), and f of the 4 updated classes (32 x 8).
-// TMA reads go to L2 (never a stale L1 line).  Consumers compute, store p
-// (+ ghost pads) with plain stores and arrive (non-blocking) on the stage's
-// named barrier; the signaler warp waits there, fences the stores to gpu
-// scope, bumps the (t, b0) completion counter and frees the stage.
+// fasmg_wave.cuh -- TMA-fed marching kernels for large levels: the 3D
+// X-MCGS half-sweep (k_sweep_tma, optionally with the coarse correction
+// fused in), the residual march (k_resid_tma: tau pass and outer norm) and
+// the 2D half-sweep (k_sweep_tma2d).  Included by fasmg_engine.cu inside
+// namespace fasmg, after fasmg_stencil.cuh.
 #pragma once
 
 // (included inside namespace fasmg; <cuda.h> for CUtensorMap is included by
 // fasmg_engine.cu at file scope)
-
-namespace wave {
-constexpr int TX = 32, TY = 8;            // tile of (b2, b1) blocks
-constexpr int HX = TX + 4, HY = TY + 1;   // halo box (cols x0-2..x0+TX+1, 9 rows)
-constexpr int HBOX = 336;                 // doubles per halo slot (324 -> 128 B multiple)
-constexpr int IBOX = TX * TY;             // interior box
-constexpr int STAGE_D = 4 * HBOX + 8 * IBOX;
-constexpr int NST = 4;                    // ring stages (named barriers 1..NST)
-constexpr int NCONS = TX * TY;            // consumer threads
-constexpr int NTHR = NCONS + 64;          // + producer warp + signaler warp
-constexpr unsigned TX_BYTES = 4u * HX * HY * 8u + 8u * IBOX * 8u;
-constexpr size_t SMEM = (size_t)NST * STAGE_D * 8 + NST * 16 + 2 * NST * 8;
-}  // namespace wave
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
@@ -84,32 +40,6 @@ __device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map,
         "l"((unsigned long long)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-struct WaveArgs {
-    double* P;
-    unsigned* flags;   // [T][B0+2][nty] per-tile-row completion counters (zeroed)
-    unsigned* ticket;  // global ticket counter (zeroed before launch)
-    int T;             // half-sweeps in this launch
-    int lag;           // planes between consecutive half-sweeps in ticket order (1 or 2)
-    unsigned odd;      // bit t: half-sweep t updates the odd-sum classes (0x96)
-    int ntx, nty;      // tiles per plane along b2, b1
-    int ng, K;         // tile groups per (t, plane), tiles per group
-    int gpr;           // groups per tile row (a group never spans rows)
-    int cyc1;          // axis 1 periodic: tile rows 0 and nty-1 are neighbours
-    long long ngroups; // total tickets
-    unsigned long long* trace;  // debug: 6 globaltimer stamps per item, or null
-};
-
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 // opposite classes of a color mask in ascending order -> slot index
 template <unsigned OPP>
@@ -118,208 +48,6 @@ __device__ __forceinline__ constexpr int oslot(int k) {
     for (int t = 0; t < k; ++t) n += (OPP >> t) & 1u;
     return n;
 }
-
-// consumer side of one item for color mask M (0x96 or 0x69)
-template <int EA, unsigned M>
-__device__ __forceinline__ void wave_item(const double* __restrict__ S, const Lvl& L,
-                                          const BcSpec& bc, double* __restrict__ P, int b0,
-                                          int x0, int y0, int tx, int ty) {
-    using namespace wave;
-    constexpr unsigned OPP = M ^ 0xFFu;
-    const double* H = S;                     // 4 halo boxes (opposite classes, plane b0)
-    const double* X = S + 4 * HBOX;          // 4 axis-0 neighbor planes
-    const double* Fb = S + 4 * HBOX + 4 * IBOX;  // f of the 4 updated classes
-    double nv[8];
-    int j = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        if (!((M >> c) & 1u)) continue;
-        const int k0 = c ^ 4, k1 = c ^ 2, k2 = c ^ 1;
-        // row of b1 in class k's halo box (start row y0 if q1(k) else y0-1)
-        const int r0 = (k0 & 2) ? ty : ty + 1;
-        const int r2 = (k2 & 2) ? ty : ty + 1;
-        const double* h0 = H + oslot<OPP>(k0) * HBOX;
-        const double* h1 = H + oslot<OPP>(k1) * HBOX;
-        const double* h2 = H + oslot<OPP>(k2) * HBOX;
-        const double cen0 = h0[r0 * HX + tx + 2];
-        const double ext0 = X[oslot<OPP>(k0) * IBOX + ty * TX + tx];
-        const double e0 = (c & 4) ? cen0 : ext0;
-        const double w0 = (c & 4) ? ext0 : cen0;
-        const double e1 = h1[(ty + 1) * HX + tx + 2];
-        const double w1 = h1[ty * HX + tx + 2];
-        const double e2 = (c & 1) ? h2[r2 * HX + tx + 2] : h2[r2 * HX + tx + 3];
-        const double w2 = (c & 1) ? h2[r2 * HX + tx + 1] : h2[r2 * HX + tx + 2];
-        // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:62)
-        const double ns = ad(ad(ad(ad(ad(e0, w0), e1), w1), e2), w2);
-        nv[c] = ad(ml(L.h2, Fb[j * IBOX + ty * TX + tx]), ml(L.b, ns));
-        ++j;
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-        if ((M >> c) & 1u) nv[c] = dv(nv[c], L.denom);
-    int bb[3] = {b0, y0 + ty, x0 + tx};
-    const bool bnd = on_boundary<3>(L, bb);
-    const long pl = at<3>(L, 0, bb[0], bb[1], bb[2]);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        if (!((M >> c) & 1u)) continue;
-        if (is_wall<3, EA>(L, c, bb)) continue;
-        const long o = pl + (long)c * L.cls;
-        P[o] = nv[c];
-        if (bnd) write_pads<3, EA>(P, L, bc, c, bb, o, nv[c]);
-    }
-}
-
-template <int EA>
-__global__ void __launch_bounds__(wave::NTHR, 2)
-    k_smooth_wave(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapI,
-                  const __grid_constant__ CUtensorMap mapF, Lvl L, BcSpec bc, WaveArgs A) {
-    using namespace wave;
-    extern __shared__ __align__(128) double sm[];
-    int4* desc = (int4*)(sm + NST * STAGE_D);
-    unsigned long long* full = (unsigned long long*)(desc + NST);
-    unsigned long long* empty = full + NST;
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int B0 = L.B[0];
-    const int pstride = B0 + 2;
-    const int ntiles = A.ntx * A.nty;
-
-    if (tid >= NCONS + 32) {  // ------------- signaler warp
-        // Publishes each finished item: waits (named barrier 1+stage) for the
-        // consumers' stores, fences them to gpu scope, bumps the item's
-        // completion counter and frees the ring stage -- so the consumers
-        // never stall on the fence.
-        int stage = 0;
-        for (;;) {
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + stage), "n"(NCONS + 32) : "memory");
-            const int4 d = desc[stage];
-            if (d.x < 0) break;
-            if (tid == NCONS + 32) {
-                // the stage's shared memory is consumed: recycle it first,
-                // then publish the item's global stores
-                mbar_arrive(&empty[stage]);
-                const int row = d.z / A.ntx;
-                __threadfence();
-                atomicAdd(A.flags + ((long)d.x * pstride + d.y) * A.nty + row, 1u);
-                if (A.trace) A.trace[6 * (((long)d.x * B0 + (d.y - 1)) * ntiles + d.z) + 5] = gtime();
-            }
-            __syncwarp();
-            if (++stage == NST) stage = 0;
-        }
-        return;
-    }
-    if (tid >= NCONS) {  // ---------------- producer warp (lane 0)
-        if (tid != NCONS) return;
-        int stage = 0;
-        unsigned ph = 1;  // empty barriers start "released"
-        const long long gpw = (long long)A.T * A.ng;
-        long long g = (long long)atomicAdd(A.ticket, 1u);
-        while (g < A.ngroups) {
-            const long long gn = (long long)atomicAdd(A.ticket, 1u);  // next ticket, in flight
-            const int w = (int)(g / gpw);
-            const int r = (int)(g - (long long)w * gpw);
-            const int t = r / A.ng, grp = r - t * A.ng;
-            const int b = w + 1 - A.lag * t;
-            g = gn;
-            if (b < 1 || b > B0) continue;
-            const unsigned long long tp0 = A.trace ? gtime() : 0ull;
-            const int row = grp / A.gpr;  // tile row of this group
-            if (t > 0) {
-                // tile rows row-1..row+1 of planes b-1..b+1 of half-sweep t-1
-                const int lo = max(1, b - 1), hi = min(B0, b + 1);
-                for (;;) {
-                    unsigned m = 0xFFFFFFFFu;
-                    for (int q = lo; q <= hi; ++q) {
-                        const unsigned* fl = A.flags + ((long)(t - 1) * pstride + q) * A.nty;
-                        for (int dr = -1; dr <= 1; ++dr) {
-                            int rr = row + dr;
-                            if (A.cyc1) rr = (rr + A.nty) % A.nty;  // periodic b1 wrap
-                            else if (rr < 0 || rr >= A.nty) continue;
-                            m = min(m, ld_acquire(fl + rr));
-                        }
-                    }
-                    if (m >= (unsigned)A.ntx) break;
-                    __nanosleep(32);
-                }
-            }
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            const unsigned long long tp1 = A.trace ? gtime() : 0ull;
-            const bool odd = (A.odd >> t) & 1u;
-            const unsigned Mk = odd ? 0x96u : 0x69u;
-            const unsigned OPP = Mk ^ 0xFFu;
-            const int c0 = (grp - row * A.gpr) * A.K;
-            const int te = row * A.ntx + min(A.ntx, c0 + A.K);
-            for (int tile = row * A.ntx + c0; tile < te; ++tile) {
-                mbar_wait(&empty[stage], ph);
-                desc[stage] = make_int4(t, b, tile, 0);
-                double* S = sm + stage * STAGE_D;
-                const int ty0 = tile / A.ntx, tx0 = tile - ty0 * A.ntx;
-                const int x0 = tx0 * TX + 1, y0 = ty0 * TY + 1;
-                mbar_expect_tx(&full[stage], TX_BYTES);
-                int n = 0, j = 0;
-                for (int k = 0; k < 8; ++k) {
-                    if ((OPP >> k) & 1u) {
-                        tma_load4(S + n * HBOX, &mapH, &full[stage], OFF + x0 - 2,
-                                  (k & 2) ? y0 : y0 - 1, b, k);
-                        tma_load4(S + 4 * HBOX + n * IBOX, &mapI, &full[stage], OFF + x0, y0,
-                                  (k & 4) ? b + 1 : b - 1, k);
-                        ++n;
-                    } else {
-                        tma_load4(S + 4 * HBOX + 4 * IBOX + j * IBOX, &mapF, &full[stage],
-                                  OFF + x0, y0, b, k);
-                        ++j;
-                    }
-                }
-                if (A.trace) {
-                    unsigned long long* tr = A.trace + 6 * (((long)t * B0 + (b - 1)) * ntiles + tile);
-                    tr[0] = tp0;
-                    tr[1] = tp1;
-                    tr[2] = gtime();
-                }
-                if (++stage == NST) { stage = 0; ph ^= 1u; }
-            }
-        }
-        // sentinel: tell the consumers (and through them the signaler) to stop
-        mbar_wait(&empty[stage], ph);
-        desc[stage] = make_int4(-1, 0, 0, 0);
-        mbar_arrive(&full[stage]);
-        return;
-    }
-
-    // ------------------------------------ consumers (8 warps)
-    const int tx = tid % TX, ty = tid / TX;
-    int stage = 0;
-    unsigned ph = 0;
-    for (;;) {
-        mbar_wait(&full[stage], ph);
-        const int4 d = desc[stage];
-        if (d.x >= 0) {
-            const int t = d.x, b = d.y, tile = d.z;
-            unsigned long long* tr =
-                A.trace ? A.trace + 6 * (((long)t * B0 + (b - 1)) * ntiles + tile) : nullptr;
-            if (tr && tid == 0) tr[3] = gtime();
-            const int ty0 = tile / A.ntx, tx0 = tile - ty0 * A.ntx;
-            const int x0 = tx0 * TX + 1, y0 = ty0 * TY + 1;
-            const double* S = sm + stage * STAGE_D;
-            if ((A.odd >> t) & 1u) wave_item<EA, 0x96u>(S, L, bc, A.P, b, x0, y0, tx, ty);
-            else wave_item<EA, 0x69u>(S, L, bc, A.P, b, x0, y0, tx, ty);
-            if (tr && tid == 0) tr[4] = gtime();
-        }
-        // hand the item to the signaler without waiting
-        asm volatile("bar.arrive %0, %1;" ::"r"(1 + stage), "n"(NCONS + 32) : "memory");
-        if (d.x < 0) break;
-        if (++stage == NST) { stage = 0; ph ^= 1u; }
-    }
-}
-
 
 // ---------------------------------------------------------------------------
 // 2.5D marching half-sweep with TMA plane loads (3D, large levels).

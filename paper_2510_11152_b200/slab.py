@@ -130,6 +130,9 @@ class _SlabEngine:
     def launch(self, count: int, with_norm: bool):
         N.call("fasmg_engine_launch", self.handle, int(count), 1 if with_norm else 0)
 
+    def prepare(self, with_norm: bool):
+        N.call("fasmg_engine_prepare", self.handle, 1 if with_norm else 0)
+
     def result(self) -> float:
         out = ctypes.c_double()
         N.call("fasmg_engine_result", self.handle, ctypes.byref(out))
@@ -186,7 +189,12 @@ class VirtualSlabSolver:
         graph launch may block the host once its stream's queue is full,
         and a rank's graph stalls on device until its peers' graphs run --
         launching the ranks one after another from one thread can deadlock
-        (observed with 8 ranks at 512^3).  ctypes releases the GIL."""
+        (observed with 8 ranks at 512^3).  ctypes releases the GIL.
+        Every rank's graph is captured first (fasmg_engine_prepare): a
+        capture that lazily loads a kernel module waits for the running
+        kernels, i.e. for peers already spinning on this rank."""
+        for e in es:
+            e.prepare(with_norm)
         if self._pool is None:
             import concurrent.futures as cf
             self._pool = cf.ThreadPoolExecutor(max_workers=self.parts)

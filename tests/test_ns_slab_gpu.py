@@ -81,7 +81,7 @@ def _single(P, n, order, dt=1e-3):
 
 @pytest.mark.parametrize("n,parts,order", [((32, 32, 32), 2, 2), ((32, 32, 32), 4, 2),
                                            ((32, 32, 32), 2, 1), ((64, 64, 64), 4, 2),
-                                           ((64, 32, 48), 2, 2)])
+                                           ((64, 32, 96), 2, 2)])
 def test_virtual_slab_ns_matches_single_gpu(P, n, parts, order):
     from paper_2510_11152_b200.ns import NSParams
     from paper_2510_11152_b200.ns_slab import SlabProjectionStepper, VirtualRanks

@@ -1,9 +1,8 @@
-"""Temporally blocked (wavefront) smoothing launches (csrc/fasmg_wave.cuh):
-bitwise parity with the CPU oracle and with the per-half-sweep path, for
-every cell/edge location, boundary kinds on every axis the wavefront
-supports, and several launch splittings (T half-sweeps per launch, K tiles
-per ticket).  The wavefront is forced onto small levels with
-FASMG_WAVE_MIN=0 so that the oracle finishes in seconds.
+"""TMA-fed marching kernels (csrc/fasmg_wave.cuh): the 3D and 2D half-sweeps
+and the coarse correction fused into the first post-smoothing half-sweep,
+forced onto small levels (FASMG_TMA_MIN=0) so that the oracle finishes in
+seconds: bitwise parity with the CPU oracle for every cell/edge location,
+boundary kinds on every axis, partial tiles and ragged march chunks.
 """
 import numpy as np
 import pytest
@@ -53,9 +52,6 @@ def bc_of(P, faces):
 
 
 def run_gpu(P, monkeypatch, env, shape, loc, faces, p0, f0, ml, k_max):
-    env = dict(env)
-    if "FASMG_WAVE_MIN" in env:
-        env.setdefault("FASMG_WAVE_T", 4)
     for k, v in env.items():
         monkeypatch.setenv(k, str(v))
     if len(set(shape)) == 1:
@@ -69,47 +65,6 @@ def run_gpu(P, monkeypatch, env, shape, loc, faces, p0, f0, ml, k_max):
                      P.make_plan("x", 3), bc_of(P, faces))
     torch.cuda.synchronize()
     return p.data.cpu().numpy(), rep
-
-
-@pytest.mark.parametrize("n,loc,spec,env", [
-    (64, "cell", "dirichlet", {"FASMG_WAVE_MIN": 0}),
-    (64, "cell", "dirichlet", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 3, "FASMG_WAVE_K": 1}),
-    (64, "cell", "dirichlet", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 1, "FASMG_WAVE_K": 7}),
-    (64, "cell", "mixed_yz", {"FASMG_WAVE_MIN": 0}),
-    (64, "cell", "neumann_x", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 5}),
-    (64, "edge_ew", "lid", {"FASMG_WAVE_MIN": 0}),
-    (64, "edge_ns", "mixed_yz", {"FASMG_WAVE_MIN": 0}),
-    (64, "edge_tb", "lid", {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 4}),
-    (128, "cell", "dirichlet", {"FASMG_WAVE_T": 8, "FASMG_WAVE_LAG": 1}),
-])
-def test_wave_vs_oracle(P, monkeypatch, n, loc, spec, env):
-    import oracle as O
-    shape = (n,) * 3
-    ml = int(np.log2(n)) - 1
-    faces = faces_of(spec)
-    p0 = C.rand_field(21, shape, loc, 1)
-    f0 = C.rand_field(22, shape, loc, 1)
-    op = O.OField(shape, loc, 1, p0.copy())
-    of = O.OField(shape, loc, 1, f0.copy())
-    O.set_threads(8)
-    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 2, 2, ml)
-    O.set_threads(1)
-    got, rep = run_gpu(P, monkeypatch, env, shape, loc, faces, p0, f0, ml, 2)
-    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
-    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
-
-
-def test_wave_matches_half_sweep_path(P, monkeypatch):
-    """Same engine inputs, wavefront on vs off: bitwise equal fields."""
-    shape = (128, 64, 64)
-    faces = faces_of("mixed_yz")
-    p0 = C.rand_field(31, shape, "cell", 1)
-    f0 = C.rand_field(32, shape, "cell", 1)
-    on, r1 = run_gpu(P, monkeypatch, {"FASMG_WAVE_MIN": 0, "FASMG_WAVE_T": 8}, shape, "cell",
-                     faces, p0, f0, 5, 3)
-    off, r2 = run_gpu(P, monkeypatch, {"FASMG_WAVE_T": 0}, shape, "cell", faces, p0, f0, 5, 3)
-    assert np.array_equal(on.view(np.uint64), off.view(np.uint64))
-    assert r1.residual_history == r2.residual_history
 
 
 @pytest.mark.parametrize("shape,loc,spec", [
@@ -137,35 +92,6 @@ def test_tma_sweep_vs_oracle(P, monkeypatch, shape, loc, spec):
                        faces, p0, f0, ml, 2)
     np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
     assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
-
-
-@pytest.mark.parametrize("shape,spec,env", [
-    ((64, 64, 64), "dirichlet", {}),
-    ((48, 112, 80), "mixed_dn", {}),                       # partial tile along b2
-    ((96, 64, 128), "mixed_dn", {"FASMG_MARCH_CHUNK": 5}),  # ragged chunks
-    ((64, 64, 64), "lid", {"FASMG_MARCH_CHUNK": 1}),
-])
-def test_fused_sweep_residual_vs_oracle(P, monkeypatch, shape, spec, env):
-    """k_sweep_resid (last half-sweep fused with the tau pass and with the
-    outer residual norm) forced onto small levels: fields bitwise equal to
-    the oracle, residual history within 1e-10."""
-    import oracle as O
-    faces = faces_of(spec)
-    ml = 3
-    p0 = C.rand_field(51, shape, "cell", 1)
-    f0 = C.rand_field(52, shape, "cell", 1)
-    op = O.OField(shape, "cell", 1, p0.copy())
-    of = O.OField(shape, "cell", 1, f0.copy())
-    O.set_threads(8)
-    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 3, 2, ml,
-                           dmin=0.0, dmax=shape[0] / shape[-1])
-    O.set_threads(1)
-    e = {"FASMG_TMA_MIN": 0, "FASMG_FUSE": 3, **env}
-    got, rep = run_gpu(P, monkeypatch, e, shape, "cell", faces, p0, f0, ml, 3)
-    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
-    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
-    off, rep2 = run_gpu(P, monkeypatch, {**e, "FASMG_FUSE": 0}, shape, "cell", faces, p0, f0, ml, 3)
-    assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
 
 
 @pytest.mark.parametrize("shape,loc,spec", [
