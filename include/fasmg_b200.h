@@ -241,6 +241,11 @@ int fasmg_engine_launch(void* engine, int count, int with_norm);
  * sharing a device is prepared before any launches (lazy module loading
  * would otherwise wait on the peers' spin-waits) */
 int fasmg_engine_prepare(void* engine, int with_norm);
+/* self-test of the sweep kernels' reciprocal division: n random normal
+ * numerators (|exponent| <= emax) x nd divisors; *bad = quotients whose bits
+ * differ from IEEE division (expected 0) */
+int fasmg_selftest_div(long n, unsigned long long seed, const double* dens, int nd, int emax,
+                       unsigned long long* bad);
 int fasmg_engine_result(void* engine, double* sumsq);
 /* test access: level geometry [cls, s0, s1, E0, E1, E2, B0, off0, G0] and a
  * device copy of a level's blocked P (which=0) or F (which=1) arrays */

@@ -61,6 +61,7 @@ struct Lvl {
     long s0, s1, cls;  // strides of block axes 0,1 (last axis stride 1)
     long nblk;         // interior blocks
     double h, h2, inv_h2, denom, a, b;
+    double rden;       // RN(1/denom) for dvr (host IEEE division)
 };
 
 template <int D>
@@ -1643,6 +1644,7 @@ static Lvl make_lvl(int dim, const int* n, int ea, double dmin, double dmax, dou
     L.a = a;
     L.b = b;
     L.denom = a * L.h2 + (double)(2 * dim) * b;
+    L.rden = 1.0 / L.denom;
     return L;
 }
 

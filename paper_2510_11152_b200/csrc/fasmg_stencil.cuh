@@ -243,7 +243,7 @@ __device__ __forceinline__ void sweep_pt(double* __restrict__ P, const double* _
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-        if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+        if ((MASK >> c) & 1u) nv[c] = dvr(nv[c], L.denom, L.rden);
     const bool bnd = on_boundary<D>(L, bb);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(256) k_sweep_pc(double* __restrict__ P,
     double ns = ad(nbv[0], nbv[1]);
 #pragma unroll
     for (int t = 2; t < 2 * D; ++t) ns = ad(ns, nbv[t]);
-    const double v = dv(ad(ml(L.h2, fv), ml(L.b, ns)), L.denom);
+    const double v = dvr(ad(ml(L.h2, fv), ml(L.b, ns)), L.denom, L.rden);
     P[o] = v;
     if (on_boundary<D>(L, bb)) write_pads<D, EA>(P, L, bc, c, bb, o, v);
 }
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256) k_sweep_march(double* __restrict__ P,
                 const double w = P[ok - (q ? sa : 0)];
                 ns = ad(ad(ns, e), w);
             }
-            nv[c] = dv(ad(ml(L.h2, fv[c]), ml(L.b, ns)), L.denom);
+            nv[c] = dvr(ad(ml(L.h2, fv[c]), ml(L.b, ns)), L.denom, L.rden);
         }
         const bool bnd = bnd_col || b0 + L.off0 == 1 || b0 + L.off0 == L.G0;
 #pragma unroll
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(256) k_sweep_smem(double* __restrict__ P,
             }
 #pragma unroll
             for (int c = 0; c < NC; ++c)
-                if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+                if ((MASK >> c) & 1u) nv[c] = dvr(nv[c], L.denom, L.rden);
             const bool bnd = on_boundary<3>(L, bb);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {

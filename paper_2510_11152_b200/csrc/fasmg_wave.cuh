@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
             }
 #pragma unroll
             for (int c = 0; c < 8; ++c)
-                if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+                if ((MASK >> c) & 1u) nv[c] = dvr(nv[c], L.denom, L.rden);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (!((MASK >> c) & 1u)) continue;
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma2d(const __grid_constant__ CUt
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-                if ((MASK >> c) & 1u) nv[c] = dv(nv[c], L.denom);
+                if ((MASK >> c) & 1u) nv[c] = dvr(nv[c], L.denom, L.rden);
             const bool bnd = on_boundary<2>(L, bb);
             const long pl = at<2>(L, 0, bb[0], bb[1], 0);
 #pragma unroll
