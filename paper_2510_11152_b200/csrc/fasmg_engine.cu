@@ -1925,10 +1925,13 @@ int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double
                       const long* fs) {
     Engine* E = (Engine*)h;
     if (E->arena && E->arena->last != E) {  // another engine used the arrays: start fresh
+        // (the finest P and F are skipped: the pack below writes their whole
+        // core box, pads included, before anything reads them)
         for (int k = 0; k < E->nl; ++k) {
             const size_t bytes = sizeof(double) * (size_t)E->L[k].cls * (1u << E->dim);
             for (double* q : {E->P[k], E->F[k], E->R[k], E->PI[k]})
-                if (q) cudaMemsetAsync(q, 0, bytes, E->stream);
+                if (q && !(k == 0 && (q == E->P[0] || q == E->F[0])))
+                    cudaMemsetAsync(q, 0, bytes, E->stream);
         }
         E->arena->last = E;
     }
