@@ -855,6 +855,8 @@ struct Engine {
     int resid_tma = 1;                  // FASMG_RESID_TMA: tau / norm on the TMA march
     int corr_fuse = 1;                  // FASMG_CORR_FUSE: correction fused into the first post half-sweep
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
+    int edge_tau = 1;                   // FASMG_EDGE_TAU: edge-field tau pass in one march (k_tau_edge_tma)
+    int etau_chunk = 8;                 // FASMG_ETAU_CHUNK: its planes per CTA
     int fuse_push = 1;                  // FASMG_FUSE_PUSH: sweeps store boundary planes into peers' halos
     // ---- coarse levels in one cluster launch (fasmg_coarse.cuh) ----
     int coarse_k0 = -1;                 // first level run by k_coarse_cycle (-1: none)
@@ -901,6 +903,16 @@ static bool corr_fused(const Engine& E, int k) {
         if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
     const unsigned m0 = E.masks[0], m1 = E.masks[1];
     return (m0 == 0x96u || m0 == 0x69u) && m1 == (m0 ^ 0xFFu);
+}
+
+// level k's edge-field tau pass runs as one TMA march (k_tau_edge_tma):
+// 3D edge field, unsharded TMA level, no periodic face
+static bool edge_tau_level(const Engine& E, int k) {
+    if (!E.edge_tau || E.dim != 3 || E.ea < 0 || !E.tma_ok[k] || E.sharded(k) || k + 1 >= E.nl)
+        return false;
+    for (int a = 0; a < 3; ++a)
+        if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
+    return true;
 }
 
 static dim3 resid_grid(const Lvl& L, int chunk) {
@@ -1297,6 +1309,14 @@ static void launch_vcycle(Engine& E, long& cnt) {
                 }
                 ++cnt;
             }
+        } else if (D == 3 && edge_tau_level(E, k)) {
+            const int ch = E.etau_chunk;
+            EA_DISPATCH(3, E.ea, (k_tau_edge_tma<(EA < 0 ? 0 : EA)><<<resid_grid(L, ch),
+                                       dim3(esw::TX, esw::TY, 1), esw::SMEM, E.stream>>>(
+                                     E.mapT[k], E.P[k], E.F[k], L, E.bc, E.bch, ch, E.P[k + 1],
+                                     E.F[k + 1], Lc, E.PI[k + 1])));
+            ++cnt;
+            launch_pad_fill<D>(E, k + 1, cnt);
         } else {
             long mc = 1;
             for (int a = 0; a < D; ++a) {
@@ -1326,7 +1346,7 @@ static void launch_vcycle(Engine& E, long& cnt) {
         }
         if (E.sharded(k + 1)) halo_exchange<D>(E, k + 1, ALL, cnt);
         else if (E.sharded(k)) gather_level<D>(E, k + 1, cnt);
-        if (E.ea >= 0) {  // pinit = R p, copied after the exchange: halo planes too
+        if (E.ea >= 0 && !(D == 3 && edge_tau_level(E, k))) {  // pinit = R p, copied after the exchange: halo planes too
             const long tot = Lc.cls * (1 << D);
             k_copy_blk<D><<<nb(tot, TPB), TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], tot);
             ++cnt;
@@ -1560,6 +1580,12 @@ static int tma_setup(Engine& E) {
     if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)rsw::SMEM));
+    if (const char* v = getenv("FASMG_EDGE_TAU")) E.edge_tau = atoi(v);
+    if (const char* v = getenv("FASMG_ETAU_CHUNK")) E.etau_chunk = std::max(1, atoi(v));
+    if (!st && E.ea >= 0)
+        EA_DISPATCH(3, E.ea, (st = fasmg_check(cudaFuncSetAttribute(
+                                  k_tau_edge_tma<(EA < 0 ? 0 : EA)>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esw::SMEM))));
     return st;
 }
 

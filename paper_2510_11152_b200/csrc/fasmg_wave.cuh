@@ -426,6 +426,320 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
 }
 
 // ---------------------------------------------------------------------------
+// Edge-field (MAC face velocity) tau pass in ONE TMA march (3D): the
+// residual r = f - A p, the (1,2,1)x(1,2,1)x(1/2) edge restriction of both r
+// and p (KER/numpy_backend.py:162-191; PKG/fas.py:99-107) and the coarse
+// outputs p_c, pinit = p_c and f_c = R(r) -- replacing k_residual_fast +
+// k_pad_all2 + 2 x k_restrict_edge_fast + the pinit copy (the r array is
+// never written).  k_coarse_src_fast then adds L_2h(p_c).
+//
+// Coarse point I (per axis) restricts fine block I: along the edge axis EA
+// both classes (columns 2I-1, 2I), along a tangential axis t the classes of
+// block I and the first class (bit 1, row 2I+1) of block I+1.  The CTA
+// computes r on its 32 x 8 tile and on the high ring the tangential in-plane
+// axes need into shared memory (Rs), evaluates the ring positions that lie
+// on a domain ghost as the homogenized BC image of r (faces, then the
+// corner from the face ghost: fill_ghosts' last-axis-first chain,
+// PKG/boundary.py:90-156) and the P box's ghost corner likewise under the
+// true BC (its face pads are kept current by the sweeps); then restricts.
+//  * EA = 0: both tangential axes (1 outer, 2 inner) are in-plane: coarse
+//    plane b0 comes from fine plane b0 (planes b0 <= B0-1; B0 holds the wall).
+//  * EA = 1, 2: the outer tangential axis is the march axis: the inner
+//    (in-plane) sums of plane b0 are carried in registers and coarse plane
+//    b0-1 completes at step b0 with the first class of plane b0 (the chunk
+//    marches one plane further; plane B0+1 is the axis-0 ghost, evaluated
+//    from plane B0's values as the BC image).
+// Arithmetic: residual as k_resid_tma (op_fast's order), restriction as
+// restrict_edge_pt -- bitwise.
+namespace esw {
+constexpr int TX = 32, TY = 8, HX = TX + 4, HB = 384;
+constexpr size_t SLOT = (size_t)8 * HB;
+constexpr size_t SMEM = (3 * SLOT) * 8 + 2 * 8;  // 2 box slots + Rs
+constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u;
+}  // namespace esw
+
+__device__ __forceinline__ double img_bc(const BcSpec& bc, int a, double v) {
+    // BC image across the HIGH face of axis a: Dirichlet 2g - v, else v
+    int k;
+    double g;
+    if (a == 0) { k = bc.kind[0][1]; g = bc.val[0][1]; }
+    else if (a == 1) { k = bc.kind[1][1]; g = bc.val[1][1]; }
+    else { k = bc.kind[2][1]; g = bc.val[2][1]; }
+    return k == BC_DIRICHLET ? sb(ml(2.0, g), v) : v;
+}
+
+template <int EA>
+__global__ void __launch_bounds__(256, 2) k_tau_edge_tma(const __grid_constant__ CUtensorMap mapH,
+                                                      double* __restrict__ P,
+                                                      const double* __restrict__ F, Lvl L,
+                                                      BcSpec bc, BcSpec bch, int chunk,
+                                                      double* __restrict__ Pc,
+                                                      double* __restrict__ Fc, Lvl Lc,
+                                                      double* __restrict__ PIc) {
+    using namespace esw;
+    static_assert(EA >= 0 && EA <= 2, "edge axis");
+    // tangential axes: outer TO, inner TI (restrict_edge_pt's P1, P2)
+    constexpr int TO = EA == 0 ? 1 : 0, TI = EA == 2 ? 1 : 2;
+    constexpr int BE = 4 >> EA, BO = 4 >> TO, BI = 4 >> TI;  // class bits
+    constexpr bool CARRY = EA != 0;  // outer axis = march axis
+    extern __shared__ __align__(128) double sm[];
+    double* Rs = sm + 2 * SLOT;
+    unsigned long long* bar = (unsigned long long*)(sm + 3 * SLOT);
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int x0 = blockIdx.x * TX + 1, y0 = blockIdx.y * TY + 1;
+    const int b0s = 1 + blockIdx.z * chunk;
+    const int b0e = min(L.B[0], b0s + chunk - 1);
+    const int B0 = L.B[0], B1 = L.B[1], B2 = L.B[2];
+    const int last = CARRY ? b0e + 1 : b0e;  // last march step
+    auto issue = [&](int b0, int s) {
+        double* S = sm + s * SLOT;
+        mbar_expect_tx(&bar[s], TXB);
+        for (int k = 0; k < 8; ++k)
+            tma_load4(S + k * HB, &mapH, &bar[s], OFF + x0 - 2, y0 - 1, b0, k);
+    };
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue(b0s, 0);
+    }
+    __syncthreads();
+    const int b1 = y0 + ty, b2 = x0 + tx;
+    const bool active = b1 <= B1 && b2 <= B2;
+    const int ci = (ty + 1) * HX + tx + 2;  // tile centre in a box
+    // residual of class c at box position q (block (b0, y0-1+q/HX, x0-2+q%HX));
+    // v0 = its across-face axis-0 neighbour (direct global load)
+    auto resid = [&](const double* S, int c, int q, double fv, double v0) {
+        const double pc = S[c * HB + q];
+        double ns = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int bit = 1 << (2 - a);
+            const bool qa = (c & bit) != 0;
+            const int k = c ^ bit;
+            const double inside = S[k * HB + q];
+            const double out = a == 0 ? v0 : S[k * HB + q + (a == 1 ? (qa ? -HX : HX) : (qa ? -1 : 1))];
+            const double e = qa ? inside : out, w = qa ? out : inside;
+            ns = a == 0 ? ad(e, w) : ad(ad(ns, e), w);
+        }
+        const double lap = ml(sb(ns, ml(6.0, pc)), L.inv_h2);
+        return sb(fv, sb(ml(L.a, pc), ml(L.b, lap)));
+    };
+    // (CARRY) inner sums of the previous plane: [cI][outer bit 1 / 0], p and r
+    double zp[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, zr[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // f and the across-face axis-0 neighbour of every class of the tile
+    // block, loaded straight from global one step AHEAD (in flight while
+    // the previous plane is restricted); the extra step needs classes 4..7
+    double fv[8], nb0[8];
+    auto load_tile = [&](int b0) {
+        const unsigned need = (CARRY && b0 == b0e + 1) ? 0xF0u : 0xFFu;
+        const long o = at<3>(L, 0, b0, b1, b2);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            fv[c] = 0.0;
+            nb0[c] = 0.0;
+            if (!active || !((need >> c) & 1u)) continue;
+            fv[c] = __ldg(F + o + (long)c * L.cls);
+            const int k = c ^ 4;
+            nb0[c] = P[o + (long)k * L.cls + ((k & 4) ? L.s0 : -L.s0)];
+        }
+    };
+    // high ring along the in-plane tangential axes: (position, class) items
+    // of the classes with the ring axis' bit set, one per thread; their f
+    // and axis-0 neighbour are loaded one step ahead too
+    constexpr int NROW = TO == 1 || TI == 1 ? TX : 0;  // ring row (axis 1)
+    constexpr int NCOL = TO == 2 || TI == 2 ? TY : 0;  // ring column (axis 2)
+    constexpr int NCOR = (NROW && NCOL) ? 1 : 0;
+    constexpr int NITEM = 4 * NROW + 4 * NCOL + 2 * NCOR;
+    int iq = -1, ic = 0;
+    double ifv = 0.0, inb = 0.0;
+    auto load_ring = [&](int b0) {
+        iq = -1;
+        if (tid >= NITEM) return;
+        const bool ext = CARRY && b0 == b0e + 1;
+        int rb1, rb2, j = tid & 3, cand;
+        if (tid < 4 * NROW) { rb1 = y0 + TY; rb2 = x0 + (tid >> 2); cand = 2; }
+        else if (tid < 4 * NROW + 4 * NCOL) { const int t = tid - 4 * NROW; rb1 = y0 + (t >> 2); rb2 = x0 + TX; cand = 1; }
+        else { rb1 = y0 + TY; rb2 = x0 + TX; cand = 3; j = tid - 4 * NROW - 4 * NCOL; }
+        // the j-th class with all `cand` bits set (and outer bit 1 on the extra step)
+        int n = 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if ((c & cand) == cand && (!ext || (c & 4))) {
+                if (n == j) ic = c;
+                ++n;
+            }
+        if (j < n && rb1 <= B1 && rb2 <= B2) {  // interior ring position
+            iq = (rb1 - (y0 - 1)) * HX + (rb2 - (x0 - 2));
+            const long o = at<3>(L, 0, b0, rb1, rb2);
+            ifv = __ldg(F + o + (long)ic * L.cls);
+            const int k = ic ^ 4;
+            inb = P[o + (long)k * L.cls + ((k & 4) ? L.s0 : -L.s0)];
+        }
+    };
+    load_tile(b0s);
+    load_ring(b0s);
+    for (int b0 = b0s; b0 <= last; ++b0) {
+        const int s = (b0 - b0s) & 1;
+        const bool ghost = CARRY && b0 == B0 + 1;       // axis-0 ghost plane
+        const bool extra = CARRY && b0 == b0e + 1;      // only outer-bit-1 classes needed
+        if (tid == 0 && b0 < last && !(CARRY && b0 + 1 == B0 + 1)) issue(b0 + 1, s ^ 1);
+        const double* S = sm + (ghost ? (s ^ 1) : s) * SLOT;  // ghost step: plane B0's box
+        double own_p[8], own_r[8];  // the tile block's p and r (regular steps)
+        if (!ghost) {
+            const unsigned cls_need = extra ? 0xF0u : 0xFFu;  // bit 0 set: classes 4..7
+            mbar_wait(&bar[s], ((b0 - b0s) >> 1) & 1);
+            if (active) {
+                // the block's 8 p values once (k_resid_tma's pattern): the
+                // inside neighbours come from registers, only the across-face
+                // in-plane ones from the box
+#pragma unroll
+                for (int c = 0; c < 8; ++c) own_p[c] = S[c * HB + ci];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    own_r[c] = 0.0;
+                    if (!((cls_need >> c) & 1u)) continue;
+                    int bb[3] = {b0, b1, b2};
+                    if (is_wall<3, EA>(L, c, bb)) continue;  // not an unknown (never restricted)
+                    double ns = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const int bit = 1 << (2 - a);
+                        const bool qa = (c & bit) != 0;
+                        const int k = c ^ bit;
+                        const double out = a == 0 ? nb0[c]
+                                                  : S[k * HB + ci + (a == 1 ? (qa ? -HX : HX) : (qa ? -1 : 1))];
+                        const double e = qa ? own_p[k] : out, w = qa ? out : own_p[k];
+                        ns = a == 0 ? ad(e, w) : ad(ad(ns, e), w);
+                    }
+                    const double lap = ml(sb(ns, ml(6.0, own_p[c])), L.inv_h2);
+                    own_r[c] = sb(fv[c], sb(ml(L.a, own_p[c]), ml(L.b, lap)));
+                    Rs[c * HB + ci] = own_r[c];
+                }
+            }
+            if (iq >= 0) Rs[ic * HB + iq] = resid(S, ic, iq, ifv, inb);
+            if (b0 < last && !(CARRY && b0 + 1 == B0 + 1)) {
+                load_tile(b0 + 1);
+                load_ring(b0 + 1);
+            }
+            __syncthreads();
+            // ghosts of the ring on the high domain faces, last axis first
+            // (faces of axis 2, then axis 1 incl. the corner): r under the
+            // homogenized bc; the P box only needs its corner (face pads are
+            // current in memory).  Only tiles touching a high face.
+            const bool gcol = NCOL && x0 + TX - 1 >= B2, grow = NROW && y0 + TY - 1 >= B1;
+            if (gcol && tid < TY + 1) {  // column B2+1
+                const int r = tid + 1, q = B2 + 1 - (x0 - 2);
+                if (y0 - 1 + r <= B1 + 1)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        if (c & 1) Rs[c * HB + r * HX + q] = img_bc(bch, 2, Rs[(c ^ 1) * HB + r * HX + q - 1]);
+            }
+            if (gcol && grow) __syncthreads();  // the corner reads the column
+            if (grow && tid < TX + 1) {  // row B1+1
+                const int r = B1 + 1 - (y0 - 1), q = tid + 2;
+                if (x0 - 2 + q <= B2 + 1)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        if (c & 2) {
+                            Rs[c * HB + r * HX + q] = img_bc(bch, 1, Rs[(c ^ 2) * HB + (r - 1) * HX + q]);
+                            if (NCOL && x0 - 2 + q == B2 + 1 && (c & 1))  // P box corner
+                                ((double*)S)[c * HB + r * HX + q] =
+                                    img_bc(bc, 1, S[(c ^ 2) * HB + (r - 1) * HX + q]);
+                        }
+            }
+            if (gcol || grow) __syncthreads();
+        }
+        // ---- restriction ----
+        // own-block values from registers, the +1 blocks along the
+        // tangential axes from Rs / the box; on the axis-0 ghost plane (CARRY,
+        // last chunk) every value is the BC image of plane B0's class c^4
+        auto rv = [&](int c, int q) {
+            return ghost ? img_bc(bch, 0, Rs[(c ^ 4) * HB + q]) : Rs[c * HB + q];
+        };
+        auto pv = [&](int c, int q) {
+            return ghost ? img_bc(bc, 0, S[(c ^ 4) * HB + q]) : S[c * HB + q];
+        };
+        // inner (1,2,1)/4 over TI: classes e|BI, e of this block and e|BI of
+        // the next block along TI (restrict_edge_pt's F(.., dk))
+        constexpr int DQ = TI == 2 ? 1 : HX;
+        auto zown = [&](const double* own, const double* A, int e) {
+            return ml(ad(ad(own[e | BI], ml(2.0, own[e])), A[(e | BI) * HB + ci + DQ]), 0.25);
+        };
+        if (!CARRY) {
+            // coarse plane b0 (edge axis 0: planes 1..B0-1); TO = 1, TI = 2
+            if (active && b0 <= B0 - 1) {
+                double res[2];
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    const double* own = w ? own_p : own_r;
+                    const double* A = w ? S : Rs;
+                    double tang[2];
+#pragma unroll
+                    for (int cI = 0; cI < 2; ++cI) {
+                        const int e = cI == 0 ? BE : 0;
+                        const double r0 = zown(own, A, e | BO);
+                        const double r1 = zown(own, A, e);
+                        // row 2J+1: class e|BO of the next block along axis 1
+                        const int q2 = ci + HX;
+                        const double r2 = ml(ad(ad(A[(e | BO | BI) * HB + q2], ml(2.0, A[(e | BO) * HB + q2])),
+                                                A[(e | BO | BI) * HB + q2 + 1]), 0.25);
+                        tang[cI] = ml(ad(ad(r0, ml(2.0, r1)), r2), 0.25);
+                    }
+                    res[w] = ml(ad(tang[0], tang[1]), 0.5);
+                }
+                int bb[3] = {b0, b1, b2}, cc = 0, cb3[3] = {0, 0, 0};
+                coarse_of<3>(L, Lc, bb, cc, cb3);
+                const long oc = at<3>(Lc, cc, cb3[0], cb3[1], cb3[2]);
+                Pc[oc] = res[1];
+                PIc[oc] = res[1];
+                Fc[oc] = res[0];
+            }
+        } else {
+            // inner sums of this plane (outer bit 1; bit 0 too except on the
+            // extra/ghost step), then coarse plane b0-1 from the carry
+            const bool edge_ok = active && (EA == 1 ? b1 <= B1 - 1 : b2 <= B2 - 1);
+            if (edge_ok) {
+                double tr[2], tp[2];
+#pragma unroll
+                for (int cI = 0; cI < 2; ++cI) {
+                    const int e = cI == 0 ? BE : 0;
+                    // row 2J+1 of coarse plane b0-1 = this plane's first
+                    // class; then this plane's sums become the carry
+                    double r1, p1;
+                    if (ghost) {
+                        const int c0 = e | BO;
+                        r1 = ml(ad(ad(rv(c0 | BI, ci), ml(2.0, rv(c0, ci))), rv(c0 | BI, ci + DQ)), 0.25);
+                        p1 = ml(ad(ad(pv(c0 | BI, ci), ml(2.0, pv(c0, ci))), pv(c0 | BI, ci + DQ)), 0.25);
+                    } else {
+                        r1 = zown(own_r, Rs, e | BO);
+                        p1 = zown(own_p, S, e | BO);
+                    }
+                    tr[cI] = ml(ad(ad(zr[cI][0], ml(2.0, zr[cI][1])), r1), 0.25);
+                    tp[cI] = ml(ad(ad(zp[cI][0], ml(2.0, zp[cI][1])), p1), 0.25);
+                    zr[cI][0] = r1;
+                    zp[cI][0] = p1;
+                    if (!extra && !ghost) {
+                        zr[cI][1] = zown(own_r, Rs, e);
+                        zp[cI][1] = zown(own_p, S, e);
+                    }
+                }
+                if (b0 > b0s) {
+                    int bb[3] = {b0 - 1, b1, b2}, cc = 0, cb3[3] = {0, 0, 0};
+                    coarse_of<3>(L, Lc, bb, cc, cb3);
+                    const long oc = at<3>(Lc, cc, cb3[0], cb3[1], cb3[2]);
+                    const double pres = ml(ad(tp[0], tp[1]), 0.5);
+                    Pc[oc] = pres;
+                    PIc[oc] = pres;
+                    Fc[oc] = ml(ad(tr[0], tr[1]), 0.5);
+                }
+            }
+        }
+        __syncthreads();  // box slot s and Rs are refilled next step
+    }
+}
+
+// ---------------------------------------------------------------------------
 // 2D half-sweep fed by TMA.  A CTA owns a 32 (b1) x 8 (b0) tile and walks
 // `steps` consecutive tiles down axis 0; per step ONE thread issues the two
 // opposite classes' tile + 1-block halo (36 x 10 box, 16-byte aligned start)

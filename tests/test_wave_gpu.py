@@ -170,3 +170,36 @@ def run_gpu_a(P, monkeypatch, env, shape, faces, p0, f0, ml, k_max, a):
                      P.make_plan("x", 3), bc_of(P, faces))
     torch.cuda.synchronize()
     return p.data.cpu().numpy(), rep
+
+
+@pytest.mark.parametrize("shape,loc,spec,env", [
+    ((64, 64, 64), "edge_ew", "lid", {}),
+    ((64, 64, 64), "edge_ns", "lid", {}),
+    ((64, 64, 64), "edge_tb", "lid", {}),
+    ((48, 112, 80), "edge_ew", "mixed_dn", {}),                      # partial tiles, Neumann faces
+    ((48, 112, 80), "edge_ns", "mixed_dn", {"FASMG_ETAU_CHUNK": 5}),  # ragged chunks
+    ((96, 48, 80), "edge_tb", "mixed_dn", {"FASMG_ETAU_CHUNK": 3}),
+    ((64, 64, 96), "edge_ns", "dirichlet", {"FASMG_ETAU_CHUNK": 1}),
+    ((64, 64, 64), "edge_tb", "lid", {"FASMG_ETAU_CHUNK": 32}),       # one chunk: the axis-0 ghost
+])
+def test_edge_tau_march_vs_oracle(P, monkeypatch, shape, loc, spec, env):
+    """Edge-field tau pass in one TMA march (k_tau_edge_tma: residual, both
+    edge restrictions, pinit), forced onto small levels: fields bitwise equal
+    to the oracle and to the unfused residual + pads + restriction kernels."""
+    import oracle as O
+    faces = faces_of(spec) if spec in FACES else C.bc_faces(3, spec)
+    ml = 3
+    p0 = C.rand_field(61, shape, loc, 1)
+    f0 = C.rand_field(62, shape, loc, 1)
+    op = O.OField(shape, loc, 1, p0.copy())
+    of = O.OField(shape, loc, 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, 1.0, 0.5, faces, O.plan_colors("x", 3), 1e-30, 2, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    e = {"FASMG_TMA_MIN": 0, **env}
+    got, rep = run_gpu(P, monkeypatch, e, shape, loc, faces, p0, f0, ml, 2)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+    off, _ = run_gpu(P, monkeypatch, {**e, "FASMG_EDGE_TAU": 0}, shape, loc, faces, p0, f0, ml, 2)
+    assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
