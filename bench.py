@@ -711,6 +711,7 @@ def ns_arm(args):
     state_bytes = (sum(v.numel() for v in hvel.values()) + hp.numel()) * 8
     clocks.stop()
     mem = torch.cuda.max_memory_allocated(dev)
+    free_b, total_b = torch.cuda.mem_get_info(dev)
     line = {
         "metric": NS_METRIC.format(n=n), "value": 1e3 / ms_step, "unit": "steps/s",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_step,
@@ -729,6 +730,7 @@ def ns_arm(args):
                        "and pressure to host; the state copies amortised over the steps"},
         "cpu_baseline": None, "clocks": clocks.summary(),
         "torch_max_allocated_gb": mem / 1e9,
+        "device_used_gb": (total_b - free_b) / 1e9,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = ns_cpu_sample(min(n, 256))

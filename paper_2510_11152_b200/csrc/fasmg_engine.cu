@@ -1788,9 +1788,11 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
             cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
         }
         if (ea >= 0) {
-            if (lvl_alloc(*E, k, 2, bytes, &E->R[k])) { delete E; return nullptr; }
+            // R[0] (the finest residual of the unfused edge tau pass) is
+            // allocated after tma_setup, only if that pass is needed
+            if (k >= 1 && lvl_alloc(*E, k, 2, bytes, &E->R[k])) { delete E; return nullptr; }
             if (k >= 1 && lvl_alloc(*E, k, 3, bytes, &E->PI[k])) { delete E; return nullptr; }
-            cudaMemsetAsync(E->R[k], 0, bytes, E->stream);
+            if (k >= 1) cudaMemsetAsync(E->R[k], 0, bytes, E->stream);
             if (k >= 1) cudaMemsetAsync(E->PI[k], 0, bytes, E->stream);
         }
         for (int t = 0; t < dim; ++t) nn[t] /= 2;
@@ -1798,6 +1800,11 @@ void* fasmg_engine_create_slab(int dim, const int* n, int ea, double dmin, doubl
     E->npart = (int)tile_ctas(tile_of(E->L[0]));
     if (int st = coarse_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (coarse cluster) failed"); return nullptr; }
     if (int st = tma_setup(*E)) { delete E; fasmg_set_error(st, "engine setup (TMA maps) failed"); return nullptr; }
+    if (ea >= 0 && !(dim == 3 && edge_tau_level(*E, 0))) {  // the unfused finest tau pass
+        const size_t bytes = sizeof(double) * (size_t)E->L[0].cls * (1u << dim);
+        if (lvl_alloc(*E, 0, 2, bytes, &E->R[0])) { delete E; return nullptr; }
+        cudaMemsetAsync(E->R[0], 0, bytes, E->stream);
+    }
     if (fasmg_check(cudaMalloc(&E->part, sizeof(double) * E->npart)) ||
         fasmg_check(cudaMalloc(&E->dsum, sizeof(double))) ||
         fasmg_check(cudaMallocHost(&E->hsum, sizeof(double))) ||

@@ -130,10 +130,22 @@ class ProjectionStepper:
             else:
                 self.slots[name] = Field(grid, LOC_OF[comp], 2, device=dev)
         self.device = next(iter(self.slots.values())).device
-        # transient scratch (not resident state, reused across components)
-        self._f = {c: Field(grid, LOC_OF[c], 1, device=self.device) for c in self.comps}
+        # transient scratch (not resident state): the momentum source of the
+        # component being solved and the pressure source are never live at
+        # the same time (every schedule runs rhs_c -> solve_c per component,
+        # then the pressure solve), so ONE buffer of the largest shape backs
+        # all of them (-3 fields: 1024^3 NS fits in well under 150 GB)
+        def shape_of(loc):
+            ea = loc.edge_axis
+            return tuple(n + 1 if a == ea else n + 2 for a, n in enumerate(grid.shape))
+        shapes = {c: shape_of(LOC_OF[c]) for c in self.comps}
+        shapes["p"] = shape_of(Location.CELL)
+        self._scratch = torch.zeros(max(int(np.prod(v)) for v in shapes.values()),
+                                    dtype=torch.float64, device=self.device)
+        view = lambda q: self._scratch[: int(np.prod(shapes[q]))].view(shapes[q])  # noqa: E731
+        self._f = {c: Field(grid, LOC_OF[c], 1, data=view(c)) for c in self.comps}
         self._mix = {}
-        self._fp = Field(grid, Location.CELL, 1, device=self.device)
+        self._fp = Field(grid, Location.CELL, 1, data=view("p"))
         self.held = {slot: q for q, slot in self.schedule.initial}  # slot -> quantity
         self.step_count = 0
         # list to collect (formula, component, start event, end event) per
