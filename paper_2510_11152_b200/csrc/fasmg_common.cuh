@@ -14,30 +14,39 @@
 
 namespace fasmg {
 
-// Thread -> point of an e0 x e1 (x e2) box without 64-bit integer division:
-// the innermost axis on blockIdx.x * blockDim.x + threadIdx.x, the outer
-// ones on blockIdx.y (and blockIdx.z).  Launch with box_grid.
-__device__ __forceinline__ bool box_coords(int dim, int e0, int e1, int e2, int* x) {
+// Thread -> points of an e0 x e1 (x e2) box without 64-bit integer division:
+// a CTA covers BOX_X points of the innermost axis x BOX_Y rows of the next
+// one, and (3D) every thread walks BOX_Z consecutive points of the outermost
+// axis, so a 512^3 box is 131K CTAs of 256 threads instead of 1M CTAs of
+// 128 (the one-point-per-thread mapping was CTA-launch-bound: k_div ran at
+// 1.9 TB/s).  Launch with box_grid / box_block and loop z < box_zn(dim).
+constexpr int BOX_X = 128, BOX_Y = 2, BOX_Z = 4;
+__host__ __device__ __forceinline__ int box_zn(int dim) { return dim == 3 ? BOX_Z : 1; }
+__device__ __forceinline__ bool box_coords(int dim, int e0, int e1, int e2, int z, int* x) {
     if (dim == 3) {
         x[2] = blockIdx.x * blockDim.x + threadIdx.x;
-        x[1] = blockIdx.y;
-        x[0] = blockIdx.z;
+        x[1] = blockIdx.y * blockDim.y + threadIdx.y;
+        x[0] = blockIdx.z * BOX_Z + z;
         return x[2] < e2 && x[1] < e1 && x[0] < e0;
     }
     x[1] = blockIdx.x * blockDim.x + threadIdx.x;
-    x[0] = blockIdx.y;
+    x[0] = blockIdx.y * blockDim.y + threadIdx.y;
     x[2] = 0;
     return x[1] < e1 && x[0] < e0;
 }
-// box_grid puts whole array extents on gridDim.y / gridDim.z, which CUDA
-// caps at 65535: callers reject larger boxes with FASMG_EINVAL up front.
+// gridDim.y / gridDim.z are capped at 65535: callers reject larger boxes
+// with FASMG_EINVAL up front.
 static inline bool box_fits(int dim, int e0, int e1) {
-    return dim == 3 ? (e0 <= 65535 && e1 <= 65535) : e0 <= 65535;
+    return dim == 3 ? ((e0 + BOX_Z - 1) / BOX_Z <= 65535 && (e1 + BOX_Y - 1) / BOX_Y <= 65535)
+                    : (e0 + BOX_Y - 1) / BOX_Y <= 65535;
 }
-static inline dim3 box_grid(int dim, int e0, int e1, int e2, int tpb) {
-    if (dim == 3) return dim3((unsigned)((e2 + tpb - 1) / tpb), (unsigned)e1, (unsigned)e0);
-    return dim3((unsigned)((e1 + tpb - 1) / tpb), (unsigned)e0, 1u);
+static inline dim3 box_grid(int dim, int e0, int e1, int e2) {
+    if (dim == 3)
+        return dim3((unsigned)((e2 + BOX_X - 1) / BOX_X), (unsigned)((e1 + BOX_Y - 1) / BOX_Y),
+                    (unsigned)((e0 + BOX_Z - 1) / BOX_Z));
+    return dim3((unsigned)((e1 + BOX_X - 1) / BOX_X), (unsigned)((e0 + BOX_Y - 1) / BOX_Y), 1u);
 }
+static inline dim3 box_block() { return dim3(BOX_X, BOX_Y, 1); }
 
 
 // ---------------------------------------------------------------------------

@@ -274,20 +274,9 @@ struct Vel3 { const double* p[3]; long s[3][3]; int n[3][3]; };
 template <int DIM, int TGT>
 __global__ void __launch_bounds__(256) k_weno_convect(double* out, S3 os, Vel3 V, int g, int e0,
                                                       int e1, int e2, double inv_2h, double eps) {
-    const long n = (long)e0 * e1 * (DIM == 3 ? e2 : 1);
-    const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= n) return;
+    for (int z = 0; z < box_zn(DIM); ++z) {
     int I[3];
-    if (DIM == 3) {
-        I[2] = (int)(t % e2);
-        const long r = t / e2;
-        I[1] = (int)(r % e1);
-        I[0] = (int)(r / e1);
-    } else {
-        I[2] = 0;
-        I[1] = (int)(t % e1);
-        I[0] = (int)(t / e1);
-    }
+    if (!box_coords(DIM, e0, e1, e2, z, I)) return;  // box mapping: no 64-bit div/mod
     const double* q = V.p[TGT];
     long qc = 0;  // q at data index I + g
 #pragma unroll
@@ -329,6 +318,7 @@ __global__ void __launch_bounds__(256) k_weno_convect(double* out, S3 os, Vel3 V
 #pragma unroll
     for (int a = 0; a < DIM; ++a) acc = ad(acc, term[a]);
     out[I3(os.s, I[0], I[1], I[2])] = acc;
+    }
 }
 
 __global__ void k_weno2(double* out, S3 os, const double* q, S3 qs, const double* wind, S3 ws,
@@ -519,16 +509,28 @@ __global__ void __launch_bounds__(256) k_chunk_sums_tree(const double* v, S3 vs,
     extern __shared__ double sh[];  // [nleaves][CH_PAD] + [nleaves]
     const long c = blockIdx.x;
     const long start = c * B;
-    for (long t = threadIdx.x; t < B; t += blockDim.x) {
-        const long q = start + t;
-        long off;
-        if (dim == 2) {
-            off = (q / e1) * vs.s[0] + (q % e1) * vs.s[1];
-        } else {
-            long k = q % e2, r = q / e2;
-            off = (r / e1) * vs.s[0] + (r % e1) * vs.s[1] + k * vs.s[2];
-        }
+    // C-order position (i0, i1, i2) of element start + t, advanced by the
+    // CTA width per iteration without 64-bit division
+    const int ne = dim == 3 ? e2 : e1;                       // innermost extent
+    long q = start + threadIdx.x;
+    long row = q / ne;
+    int col = (int)(q - row * ne);
+    long i0 = dim == 3 ? row / e1 : row;
+    int i1 = dim == 3 ? (int)(row - i0 * e1) : col;
+    const int step = blockDim.x;
+    for (long t = threadIdx.x; t < B; t += step) {
+        const long off = dim == 3 ? i0 * vs.s[0] + (long)i1 * vs.s[1] + (long)col * vs.s[2]
+                                  : i0 * vs.s[0] + (long)col * vs.s[1];
         sh[(t / CH_LEAF) * CH_PAD + (t % CH_LEAF)] = v[off];
+        col += step;
+        while (col >= ne) {
+            col -= ne;
+            if (dim == 3) {
+                if (++i1 == e1) { i1 = 0; ++i0; }
+            } else {
+                ++i0;
+            }
+        }
     }
     __syncthreads();
     double* leaf = sh + (long)nleaves * CH_PAD;
@@ -594,35 +596,41 @@ __global__ void k_pw_sumsq_level(const double* v, S3 vs, int dim, int e1, int e2
     scratch[(1L << d) - 1 + t] = res;
 }
 
-__global__ void k_chunk_total(const double* sums, long nchunks, double* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// (the whole CTA stages batches of sums in shared memory with coalesced
+// loads; thread 0 adds them in chunk order -- the adds are inherently
+// serial, the loads no longer are)
+constexpr int CT_BATCH = 4096;
+__global__ void __launch_bounds__(1024) k_chunk_total(const double* sums, long nchunks,
+                                                      double* out) {
+    __shared__ double sh[CT_BATCH];
     double acc = 0.0;
-    long c = 0;
-    for (; c + 8 <= nchunks; c += 8) {  // loads issued ahead of the serial adds
-        double x[8];
+    for (long c0 = 0; c0 < nchunks; c0 += CT_BATCH) {
+        const int nb = (int)min((long)CT_BATCH, nchunks - c0);
+        for (int j = threadIdx.x; j < nb; j += blockDim.x) sh[j] = sums[c0 + j];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int j = 0;
+            for (; j + 8 <= nb; j += 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = sums[c + j];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc = ad(acc, x[j]);
+                for (int u = 0; u < 8; ++u) acc = ad(acc, sh[j + u]);
+            }
+            for (; j < nb; ++j) acc = ad(acc, sh[j]);
+        }
+        __syncthreads();
     }
-    for (; c < nchunks; ++c) acc = ad(acc, sums[c]);
-    out[0] = acc;
+    if (threadIdx.x == 0) out[0] = acc;
 }
 
 // interior -= scalar (device scalar: out[0] / count)
 __global__ void k_sub_mean(double* v, S3 vs, int dim, int e0, int e1, int e2,
                            const double* total, double count) {
-    long n = (long)e0 * e1 * (dim == 3 ? e2 : 1);
-    long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    double m = dv(total[0], count);
-    long off;
-    if (dim == 2) off = (t / e1) * vs.s[0] + (t % e1) * vs.s[1];
-    else {
-        long k = t % e2, r = t / e2;
-        off = (r / e1) * vs.s[0] + (r % e1) * vs.s[1] + k * vs.s[2];
+    const double m = dv(total[0], count);
+    for (int z = 0; z < box_zn(dim); ++z) {
+        int x[3];
+        if (!box_coords(dim, e0, e1, e2, z, x)) return;
+        const long off = I3(vs.s, x[0], x[1], x[2]);
+        v[off] = sb(v[off], m);
     }
-    v[off] = sb(v[off], m);
 }
 
 
@@ -655,17 +663,19 @@ __global__ void k_grad(const double* p, S3 ps, double* out, int dim, int axis, i
 struct Comps { const double* c[3]; S3 s[3]; };
 __global__ void k_div(Comps C, double* out, S3 os, int dim, int n0, int n1, int n2,
                       double inv_h) {
-    int x[3];
-    if (!box_coords(dim, n0, n1, n2, x)) return;  // 0-based interior box position
-    const int y0 = x[0] + 1, y1 = x[1] + 1, y2 = dim == 3 ? x[2] + 1 : 0;
-    double acc = 0.0;
-    for (int a = 0; a < dim; ++a) {
-        long hi = I3(C.s[a].s, y0, y1, y2);
-        long lo = hi - C.s[a].s[a];
-        double term = ml(sb(C.c[a][hi], C.c[a][lo]), inv_h);
-        acc = a == 0 ? term : ad(acc, term);
+    for (int z = 0; z < box_zn(dim); ++z) {
+        int x[3];
+        if (!box_coords(dim, n0, n1, n2, z, x)) return;  // 0-based interior box position
+        const int y0 = x[0] + 1, y1 = x[1] + 1, y2 = dim == 3 ? x[2] + 1 : 0;
+        double acc = 0.0;
+        for (int a = 0; a < dim; ++a) {
+            long hi = I3(C.s[a].s, y0, y1, y2);
+            long lo = hi - C.s[a].s[a];
+            double term = ml(sb(C.c[a][hi], C.c[a][lo]), inv_h);
+            acc = a == 0 ? term : ad(acc, term);
+        }
+        out[I3(os.s, x[0], x[1], dim == 3 ? x[2] : 0)] = acc;
     }
-    out[I3(os.s, x[0], x[1], dim == 3 ? x[2] : 0)] = acc;
 }
 
 // ------------------------------------------------ projection-step elementwise
@@ -689,8 +699,9 @@ struct V4 { const double* p[4]; S3 s[4]; };
 
 __global__ void k_ns_elem(int op, double* out, S3 os, V4 in, double s0, double s1, int dim,
                           int e0, int e1, int e2) {
+    for (int z = 0; z < box_zn(dim); ++z) {
     int x[3];
-    if (!box_coords(dim, e0, e1, e2, x)) return;
+    if (!box_coords(dim, e0, e1, e2, z, x)) return;
     double v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -708,6 +719,7 @@ __global__ void k_ns_elem(int op, double* out, S3 os, V4 in, double s0, double s
         default: r = -v[0]; break;
     }
     out[I3(os.s, x[0], x[1], x[2])] = r;
+    }
 }
 
 // Momentum source of one velocity component in ONE pass (the order-1 /
@@ -721,8 +733,9 @@ __global__ void k_ns_rhs(int order, double* out, S3 os, const double* u, S3 us,
                          const double* conv, S3 cs, const double* p, S3 ps, int dim, int axis,
                          int m0, int m1, int m2, double s0, double s1, double inv_h,
                          double inv_h2) {
+    for (int zz = 0; zz < box_zn(dim); ++zz) {
     int x[3];
-    if (!box_coords(dim, m0, m1, m2, x)) return;
+    if (!box_coords(dim, m0, m1, m2, zz, x)) return;
     const int z = dim == 3 ? 1 : 0;
     x[0] += 1;
     x[1] += 1;
@@ -745,6 +758,7 @@ __global__ void k_ns_rhs(int order, double* out, S3 os, const double* u, S3 us,
         r = ad(r, ml(s1, lap));
     }
     out[I3(os.s, x[0] - 1, x[1] - 1, x[2] - z)] = r;
+    }
 }
 
 // 5/7-point Laplacian (nsum - 2d*c) * inv_h2 (KER/numpy_backend.py:66-88)
@@ -953,15 +967,16 @@ int fasmg_weno_convect(double* out, const long* os, const double* const* vel, co
     const long n = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
     if (target < 0 || target >= dim) return fasmg_set_error(FASMG_EINVAL, "bad target axis");
     const int e2 = dim == 3 ? ext[2] : 1;
-    const unsigned nb = nblk(n, TPB);
+    if (!box_fits(dim, ext[0], ext[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
+    const dim3 nb = box_grid(dim, ext[0], ext[1], e2), tb = box_block();
     if (n > 0) {
         if (dim == 2) {
-            if (target == 0) k_weno_convect<2, 0><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
-            else k_weno_convect<2, 1><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            if (target == 0) k_weno_convect<2, 0><<<nb, tb, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            else k_weno_convect<2, 1><<<nb, tb, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
         } else {
-            if (target == 0) k_weno_convect<3, 0><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
-            else if (target == 1) k_weno_convect<3, 1><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
-            else k_weno_convect<3, 2><<<nb, TPB, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            if (target == 0) k_weno_convect<3, 0><<<nb, tb, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            else if (target == 1) k_weno_convect<3, 1><<<nb, tb, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
+            else k_weno_convect<3, 2><<<nb, tb, 0, S(stream)>>>(out, o, V, g, ext[0], ext[1], e2, inv_2h, eps);
         }
     }
     return fasmg_check_launch();
@@ -1101,7 +1116,7 @@ int fasmg_view_chunk_sums(const double* v, const long* vs, int dim, const int* e
 
 // Sequential total of nch chunk sums in chunk order into out[0] (device).
 int fasmg_chunk_total(const double* sums, long nch, double* out, void* stream) {
-    k_chunk_total<<<1, 32, 0, S(stream)>>>(sums, nch, out);
+    k_chunk_total<<<1, 1024, 0, S(stream)>>>(sums, nch, out);
     return fasmg_check_launch();
 }
 
@@ -1174,9 +1189,10 @@ int fasmg_sub_mean(double* v, const long* vs, int dim, const int* ext, const dou
     long n = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
     S3 s = mk(vs);
     if (dim == 2) s.s[2] = 0;
-    LAUNCH(n, (k_sub_mean<<<nblk(n, TPB), TPB, 0, S(stream)>>>(v, s, dim, ext[0], ext[1],
-                                                               dim == 3 ? ext[2] : 1, total,
-                                                               count)));
+    if (!box_fits(dim, ext[0], ext[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
+    LAUNCH(n, (k_sub_mean<<<box_grid(dim, ext[0], ext[1], dim == 3 ? ext[2] : 1), box_block(), 0,
+                            S(stream)>>>(v, s, dim, ext[0], ext[1], dim == 3 ? ext[2] : 1, total,
+                                         count)));
 }
 
 // gradient_axis: p core view; out contiguous interior of the axis' edge field
@@ -1205,7 +1221,7 @@ int fasmg_divergence(const double* const* comps, const long* cs, double* out, co
     if (dim == 2) o.s[2] = 0;
     if (!box_fits(dim, n[0], n[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
     long tot = (long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
-    LAUNCH(tot, (k_div<<<box_grid(dim, n[0], n[1], dim == 3 ? n[2] : 1, 128), 128, 0,
+    LAUNCH(tot, (k_div<<<box_grid(dim, n[0], n[1], dim == 3 ? n[2] : 1), box_block(), 0,
                          S(stream)>>>(C, out, o, dim, n[0], n[1], dim == 3 ? n[2] : 1, inv_h)));
 }
 
@@ -1223,7 +1239,7 @@ int fasmg_ns_elem(int op, double* out, const long* os, const double* const* in,
     if (dim == 2) o.s[2] = 0;
     if (!box_fits(dim, ext[0], ext[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
     long tot = (long)ext[0] * ext[1] * (dim == 3 ? ext[2] : 1);
-    LAUNCH(tot, (k_ns_elem<<<box_grid(dim, ext[0], ext[1], dim == 3 ? ext[2] : 1, 128), 128, 0,
+    LAUNCH(tot, (k_ns_elem<<<box_grid(dim, ext[0], ext[1], dim == 3 ? ext[2] : 1), box_block(), 0,
                              S(stream)>>>(op, out, o, v, s0, s1, dim, ext[0], ext[1],
                                           dim == 3 ? ext[2] : 1)));
 }
@@ -1239,7 +1255,7 @@ int fasmg_ns_rhs(int order, double* out, const long* os, const double* ucore, co
     if (dim == 2) { o.s[2] = 0; uu.s[2] = 0; cc.s[2] = 0; pp.s[2] = 0; }
     if (!box_fits(dim, m[0], m[1])) return fasmg_set_error(FASMG_EINVAL, "extent exceeds the 65535 CUDA grid-dimension limit of this launch");
     long tot = (long)m[0] * m[1] * (dim == 3 ? m[2] : 1);
-    LAUNCH(tot, (k_ns_rhs<<<box_grid(dim, m[0], m[1], dim == 3 ? m[2] : 1, 128), 128, 0,
+    LAUNCH(tot, (k_ns_rhs<<<box_grid(dim, m[0], m[1], dim == 3 ? m[2] : 1), box_block(), 0,
                             S(stream)>>>(
                      order, out, o, ucore, uu, conv, cc, pcore, pp, dim, axis, m[0], m[1],
                      dim == 3 ? m[2] : 1, s0, s1, inv_h, inv_h2)));

@@ -30,5 +30,5 @@ for ev in prof.events():
         a[1] += ev.device_time_total / 1e3 if hasattr(ev, "device_time_total") else ev.cuda_time_total / 1e3
 tot = sum(a[1] for a in agg.values())
 print(f"{n}^3 order {order}: {steps} steps, device kernel time {tot / steps:.1f} ms/step")
-for nm, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
+for nm, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:45]:
     print(f"  {nm:48s} x{c / steps:7.1f}/step {t / steps:8.2f} ms/step")
