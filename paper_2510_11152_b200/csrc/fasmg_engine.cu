@@ -503,14 +503,19 @@ template <int D>
 __device__ __forceinline__ void corr_edge_pt(const double* __restrict__ Pc,
                                              const double* __restrict__ PI, const Lvl& Lc,
                                              const BcSpec& bch, double* __restrict__ Corr,
-                                             const int* b) {
+                                             const int* b, bool skip_inner = false) {
     const long o0 = at<D>(Lc, 0, b[0], b[1], b[2]);
     CorrReader<D> rd{Pc, PI, Lc};
+    // (skip_inner: the interior points of interior blocks are k_corr_edge_in's)
+    bool inner_blk = skip_inner;
+#pragma unroll
+    for (int a = 0; a < D; ++a) inner_blk = inner_blk && b[a] >= 1 && b[a] <= Lc.B[a];
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
         int x[3] = {0, 0, 0};
         bool in;
         if (!grid_idx<D>(Lc, c, b, x, &in)) continue;
+        if (inner_blk && in) continue;
         const long o = o0 + (long)c * Lc.cls;
         double v;
         if (in) {
@@ -528,10 +533,31 @@ __device__ __forceinline__ void corr_edge_pt(const double* __restrict__ Pc,
     }
 }
 
+// The interior part of Corr (the common case of corr_edge_pt), on the block
+// tile of the coarse level's interior blocks: one subtraction per interior
+// point, without the ghost chain's registers and stack frame.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_corr_edge_in(const double* __restrict__ Pc,
+                                                      const double* __restrict__ PI, Lvl Lc,
+                                                      double* __restrict__ Corr) {
+    int bb[3];
+    if (!tile_coords<D>(Lc, bb)) return;
+    const long o0 = at<D>(Lc, 0, bb[0], bb[1], bb[2]);
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) {
+        int x[3] = {0, 0, 0};
+        bool in;
+        if (!grid_idx<D>(Lc, c, bb, x, &in) || !in) continue;
+        const long o = o0 + (long)c * Lc.cls;
+        Corr[o] = sb(Pc[o], PI[o]);
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc,
                                                    const double* __restrict__ PI, Lvl Lc,
-                                                   BcSpec bch, double* __restrict__ Corr) {
+                                                   BcSpec bch, double* __restrict__ Corr,
+                                                   int skip_inner = 0) {
     int b[3] = {0, 0, 0};
     if (D == 3) {
         b[2] = blockIdx.x * blockDim.x + threadIdx.x;
@@ -543,7 +569,41 @@ __global__ void __launch_bounds__(TPB) k_corr_edge(const double* __restrict__ Pc
         b[0] = blockIdx.y * blockDim.y + threadIdx.y;
         if (b[1] >= Lc.E[1] || b[0] >= Lc.E[0]) return;
     }
-    corr_edge_pt<D>(Pc, PI, Lc, bch, Corr, b);
+    corr_edge_pt<D>(Pc, PI, Lc, bch, Corr, b, skip_inner != 0);
+}
+
+// The non-interior part of Corr (ghost chain): only the block positions on
+// the six faces of the block box (0 or B+1 along an axis) and, for an edge
+// field, the high wall plane (block B along the edge axis, whose class-0
+// points are the wall) -- grid (x, y) over the other two axes, z = plane.
+template <int D>
+__global__ void __launch_bounds__(TPB) k_corr_edge_pads(const double* __restrict__ Pc,
+                                                        const double* __restrict__ PI, Lvl Lc,
+                                                        BcSpec bch, double* __restrict__ Corr) {
+    const int z = blockIdx.z;
+    int a, pos;
+    if (z < 2 * D) {
+        a = z >> 1;
+        pos = (z & 1) ? Lc.B[a] + 1 : 0;
+    } else {
+        a = Lc.ea;  // the wall plane (launched for edge fields only)
+        pos = Lc.B[a];
+    }
+    int oth[2] = {0, 0}, no = 0;
+    for (int t = 0; t < D; ++t)
+        if (t != a) oth[no++] = t;
+    int b[3] = {0, 0, 0};
+    b[a] = pos;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (D == 3) {
+        b[oth[0]] = blockIdx.y;
+        b[oth[1]] = i;
+        if (b[oth[0]] >= Lc.E[oth[0]] || b[oth[1]] >= Lc.E[oth[1]]) return;
+    } else {
+        b[oth[0]] = i;
+        if (blockIdx.y || b[oth[0]] >= Lc.E[oth[0]]) return;
+    }
+    corr_edge_pt<D>(Pc, PI, Lc, bch, Corr, b, true);
 }
 
 // launch geometry of k_corr_edge: every block position 0..E-1 per axis
@@ -1374,8 +1434,17 @@ static void launch_vcycle(Engine& E, long& cnt) {
             if (E.edge_fast) {
                 dim3 cg, cbk;
                 corr_edge_grid<D>(Lc, cg, cbk);
-                k_corr_edge<D><<<cg, cbk, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc, E.bch,
-                                                         E.R[k + 1]);
+                const Tile tcc = tile_of(Lc);
+                k_corr_edge_in<D><<<tcc.grid, tcc.block, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1],
+                                                                         Lc, E.R[k + 1]);
+                {
+                    int mx = 1;
+                    for (int a = 0; a < D; ++a) mx = std::max(mx, Lc.E[a]);
+                    const dim3 pg((mx + TPB - 1) / TPB, D == 3 ? mx : 1, 2 * D + 1);
+                    k_corr_edge_pads<D><<<pg, TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc,
+                                                                  E.bch, E.R[k + 1]);
+                }
+                ++cnt;
                 EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<t.grid, t.block, 0,
                                                                    E.stream>>>(E.P[k], L,
                                                                                E.R[k + 1], Lc)));
