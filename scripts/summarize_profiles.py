@@ -6,7 +6,7 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 dim = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 go = os.path.join(root, "gpurun_out")
-prof = os.path.join(root, "profiles")
+prof = os.environ.get("PROF_OUT", os.path.join(root, "profiles"))
 os.makedirs(prof, exist_ok=True)
 out = []
 
@@ -74,12 +74,15 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
         "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
         "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
-for kind in ("sweep", "tau"):
+for kind in ("sweep", "tau", "corr", "etau"):
     rep = os.path.join(go, f"{tag}_{kind}.ncu-rep")
     if not os.path.exists(rep):
         continue
     v, u = raw(rep)
-    out.append(f"\n# {tag}: ncu --set full, one {kind} launch (finest level)")
+    label = {"sweep": "finest half-sweep (k_sweep_tma)", "tau": "finest tau pass (k_resid_tma<1>)",
+             "corr": "finest corrected half-sweep (k_sweep_tma<.., CORR>)",
+             "etau": "finest edge-field tau pass (k_tau_edge_tma, EDGE_NS)"}[kind]
+    out.append(f"\n# {tag}: ncu --set full, one launch: {label}")
     for k in want:
         if k in v:
             out.append(f"{k:60s} {v[k]} {u.get(k, '')}")
