@@ -274,50 +274,66 @@ struct Vel3 { const double* p[3]; long s[3][3]; int n[3][3]; };
 template <int DIM, int TGT>
 __global__ void __launch_bounds__(256) k_weno_convect(double* out, S3 os, Vel3 V, int g, int e0,
                                                       int e1, int e2, double inv_2h, double eps) {
-    for (int z = 0; z < box_zn(DIM); ++z) {
+    // the thread's first point (box mapping, no 64-bit div/mod); every
+    // address below is a per-thread base advanced by the axis-0 stride for
+    // each further point of the z walk
     int I[3];
-    if (!box_coords(DIM, e0, e1, e2, z, I)) return;  // box mapping: no 64-bit div/mod
+    if (!box_coords(DIM, e0, e1, e2, 0, I)) return;
     const double* q = V.p[TGT];
     long qc = 0;  // q at data index I + g
 #pragma unroll
     for (int b = 0; b < DIM; ++b) qc += (long)(I[b] + g) * V.s[TGT][b];
-    // every load first (5 q values per axis, 4 wind values per foreign axis),
-    // then the per-axis WENO points (independent), then the ordered sum
-    double qv[DIM][5], w[DIM];
+    const double* qp = q + qc;
+    // wind of a foreign axis a: core index of vel[a] is target axis I+1+dt,
+    // own axis I+da, else I+1; data index = core + g - 1
+    const double* wp[DIM];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-#pragma unroll
-        for (int d = 0; d < 5; ++d) qv[a][d] = q[qc + (long)(d - 2) * V.s[TGT][a]];
-    }
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-        if (a == TGT) continue;
-        // core index of vel[a]: target axis I+1+dt, own axis I+da, else I+1;
-        // data index = core + g - 1
         long base = 0;
 #pragma unroll
         for (int b = 0; b < DIM; ++b) {
             const int c = b == TGT ? I[b] + 1 : (b == a ? I[b] : I[b] + 1);
             base += (long)(c + g - 1) * V.s[a][b];
         }
-        const double* va = V.p[a];
-        const long st = V.s[a][TGT], sa = V.s[a][a];
-        const double v00 = va[base], v01 = va[base + sa], v10 = va[base + st],
-                     v11 = va[base + st + sa];
-        w[a] = ml(0.25, ad(ad(v00, v01), ad(v10, v11)));  // PKG/weno.py:51
+        wp[a] = V.p[a] + base;
     }
-    w[TGT] = qv[0][2];
-    double term[DIM];
+    double* op = out + I3(os.s, I[0], I[1], I[2]);
+    const int nz = DIM == 3 ? min(BOX_Z, e0 - I[0]) : 1;
+    for (int z = 0; z < nz; ++z) {
+        // every load first (5 q values per axis, 4 wind values per foreign
+        // axis), then the per-axis WENO points (independent), then the
+        // ordered sum
+        double qv[DIM][5], w[DIM];
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-        const double dm2 = sb(qv[a][1], qv[a][0]), dm1 = sb(qv[a][2], qv[a][1]);
-        const double dp1 = sb(qv[a][3], qv[a][2]), dp2 = sb(qv[a][4], qv[a][3]);
-        term[a] = ml(w[a], weno_point(dm2, dm1, dp1, dp2, w[a], inv_2h, eps));
-    }
-    double acc = 0.0;
+        for (int a = 0; a < DIM; ++a) {
+            const long sa = V.s[TGT][a];
 #pragma unroll
-    for (int a = 0; a < DIM; ++a) acc = ad(acc, term[a]);
-    out[I3(os.s, I[0], I[1], I[2])] = acc;
+            for (int d = 0; d < 5; ++d) qv[a][d] = qp[(d - 2) * sa];
+        }
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            if (a == TGT) continue;
+            const long st = V.s[a][TGT], sa = V.s[a][a];
+            const double* va = wp[a];
+            const double v00 = va[0], v01 = va[sa], v10 = va[st], v11 = va[st + sa];
+            w[a] = ml(0.25, ad(ad(v00, v01), ad(v10, v11)));  // PKG/weno.py:51
+        }
+        w[TGT] = qv[0][2];
+        double term[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            const double dm2 = sb(qv[a][1], qv[a][0]), dm1 = sb(qv[a][2], qv[a][1]);
+            const double dp1 = sb(qv[a][3], qv[a][2]), dp2 = sb(qv[a][4], qv[a][3]);
+            term[a] = ml(w[a], weno_point(dm2, dm1, dp1, dp2, w[a], inv_2h, eps));
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) acc = ad(acc, term[a]);
+        *op = acc;
+        qp += V.s[TGT][0];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) wp[a] += V.s[a][0];
+        op += os.s[0];
     }
 }
 
