@@ -916,6 +916,7 @@ struct Engine {
     int corr_fuse = 1;                  // FASMG_CORR_FUSE: correction fused into the first post half-sweep
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
     int edge_tau = 1;                   // FASMG_EDGE_TAU: edge-field tau pass in one march (k_tau_edge_tma)
+    int resid_pf = 1;                   // FASMG_RESID_PF: tau/norm marches load f and the axis-0 plane a step ahead
     int etau_chunk = 8;                 // FASMG_ETAU_CHUNK: its planes per CTA
     int fuse_push = 1;                  // FASMG_FUSE_PUSH: sweeps store boundary planes into peers' halos
     // ---- coarse levels in one cluster launch (fasmg_coarse.cuh) ----
@@ -1358,6 +1359,12 @@ static void launch_vcycle(Engine& E, long& cnt) {
             {
                 if (D == 3 && resid_tma_level(E, k)) {
                     const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+                    if (E.resid_pf)
+                        k_resid_tma<1, -1, true><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1),
+                                                   rsw::SMEM, E.stream>>>(
+                            E.mapT[k], E.P[k], E.F[k], L, E.bc, ch, nullptr, E.P[k + 1],
+                            E.F[k + 1], Lc, corr_fused(E, k) ? E.PI[k + 1] : nullptr);
+                    else
                     k_resid_tma<1><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1), rsw::SMEM,
                                      E.stream>>>(E.mapT[k], E.P[k], E.F[k], L, E.bc, ch,
                                                  nullptr, E.P[k + 1], E.F[k + 1], Lc,
@@ -1470,6 +1477,12 @@ static void launch_norm(Engine& E, long& cnt) {
         if (D == 3 && E.resid_tma && E.tma_ok[0] && !E.sharded(0)) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
+            if (E.resid_pf)
+                EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA, true><<<g, dim3(rsw::TX, rsw::TY, 1),
+                                                                 E.norm_smem, E.stream>>>(
+                                         E.mapT[0], E.P[0], E.F[0], L, E.bc, ch, E.part, nullptr,
+                                         nullptr, L, nullptr)));
+            else
             EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA><<<g, dim3(rsw::TX, rsw::TY, 1), E.norm_smem,
                                                        E.stream>>>(
                                      E.mapT[0], E.P[0], E.F[0], L, E.bc, ch, E.part, nullptr,
@@ -1646,10 +1659,18 @@ static int tma_setup(Engine& E) {
                                         k_resid_tma<0, EA>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         E.norm_smem))));
+    if (!st) EA_DISPATCH(3, E.ea, (st = fasmg_check(cudaFuncSetAttribute(
+                                        k_resid_tma<0, EA, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        E.norm_smem))));
     if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)rsw::SMEM));
+    if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1, -1, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)rsw::SMEM));
     if (const char* v = getenv("FASMG_EDGE_TAU")) E.edge_tau = atoi(v);
+    if (const char* v = getenv("FASMG_RESID_PF")) E.resid_pf = atoi(v);
     if (const char* v = getenv("FASMG_ETAU_CHUNK")) E.etau_chunk = std::max(1, atoi(v));
     if (!st && E.ea >= 0)
         EA_DISPATCH(3, E.ea, (st = fasmg_check(cudaFuncSetAttribute(

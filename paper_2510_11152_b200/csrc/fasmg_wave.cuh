@@ -317,7 +317,7 @@ constexpr size_t SMEM = 2 * SLOT * 8 + 2 * 8;
 constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u;
 }  // namespace rsw
 
-template <int MODE, int EA = -1>
+template <int MODE, int EA = -1, bool RESID_PF = false>
 __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUtensorMap mapH,
                                                    const double* __restrict__ P,
                                                    const double* __restrict__ F, Lvl L,
@@ -350,20 +350,24 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
     const bool active = b1 <= L.B[1] && b2 <= L.B[2];
     const int ci = (ty + 1) * HX + tx + 2;  // tile centre in a halo box
     double acc = 0.0;
+    // f and the axis-0 neighbour plane of every class straight from global
+    // (coalesced rows, L2-resident), loaded one plane step AHEAD so their
+    // latency hides behind the current plane's arithmetic (RESID_PF)
+    double fv[8], nb0[8];
+    auto load_tile = [&](int b0) {
+        if (!active) return;
+        const long o = at<3>(L, 0, b0, b1, b2);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            fv[c] = __ldg(F + o + (long)c * L.cls);
+            nb0[c] = P[o + (long)c * L.cls + ((c & 4) ? L.s0 : -L.s0)];
+        }
+    };
+    if (RESID_PF) load_tile(b0s);
     for (int b0 = b0s; b0 <= b0e; ++b0) {
         const int s = (b0 - b0s) & 1;
         if (tid == 0 && b0 < b0e) issue(b0 + 1, s ^ 1);
-        // f and the axis-0 neighbour plane of every class straight from global
-        // (coalesced rows, L2-resident), issued before the barrier wait
-        double fv[8], nb0[8];
-        if (active) {
-            const long o = at<3>(L, 0, b0, b1, b2);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                fv[c] = __ldg(F + o + (long)c * L.cls);
-                nb0[c] = P[o + (long)c * L.cls + ((c & 4) ? L.s0 : -L.s0)];
-            }
-        }
+        if (!RESID_PF) load_tile(b0);  // issued before the barrier wait
         mbar_wait(&bar[s], ((b0 - b0s) >> 1) & 1);
         const double* S = sm + s * SLOT;
         if (active) {
@@ -411,6 +415,7 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                 if (on_boundary<3>(Lc, cb)) write_pads<3, -1>(Pc, Lc, bc, cc, cb, oc, pcv);
             }
         }
+        if (RESID_PF && b0 < b0e) load_tile(b0 + 1);
         __syncthreads();  // slot s is refilled by the next step's prefetch
     }
     if (MODE == 0) {
