@@ -215,12 +215,26 @@ class FasSolver:
         return SolveReport(iterations=len(history), residual_history=history,
                            converged=bool(history and history[-1] <= params.tol))
 
-    def _solve(self, p: Field, f: Field, params: FasParams) -> list:
+    def solve_into(self, p0: Field, p: Field, f: Field, params: FasParams) -> SolveReport:
+        """``solve`` with the initial guess read from ``p0`` and the solution
+        (ghosts filled) written to ``p`` -- bitwise ``p.data.copy_(p0.data);
+        solve(p, f, params)`` without the copy: the engine packs ``p0``
+        directly, and every element of ``p`` is rewritten (interior by the
+        store, the rest by fill_ghosts).  Used by the NS drivers, whose
+        momentum solves start from u^n and write u~ into another slot."""
+        self._check(p0, f)
+        self._check(p, f)
+        with torch.cuda.device(p.device):
+            history = self._solve(p, f, params, p0=p0)
+        return SolveReport(iterations=len(history), residual_history=history,
+                           converged=bool(history and history[-1] <= params.tol))
+
+    def _solve(self, p: Field, f: Field, params: FasParams, p0: Field | None = None) -> list:
         singular = self._singular()
         if singular:
             subtract_interior_mean(f)
         e = self.engine(params.s, p.device)
-        e.load(p, f)
+        e.load(p if p0 is None else p0, f)
         g = self.hierarchy.fine
         scale = g.h ** (g.dim / 2.0)
         history: list = []

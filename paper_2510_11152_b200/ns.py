@@ -292,9 +292,8 @@ class ProjectionStepper:
             q, slot = st.writes[0]
             dst = self.slots[slot]
             src = read[f"{c}_n"]
-            if dst is not src:
-                dst.data.copy_(src.data)
-            rep.momentum[c] = self.solvers[c].solve(dst, read[f"f_{c}"], self.fas)
+            # the solve starts from u^n and writes u~ into the slot (no copy)
+            rep.momentum[c] = self.solvers[c].solve_into(src, dst, read[f"f_{c}"], self.fas)
             self._bind(q, slot)
         elif st.formula == "solve_pressure":
             q, slot = st.writes[0]
