@@ -560,6 +560,46 @@ __global__ void __launch_bounds__(256) k_chunk_sums_tree(const double* v, S3 vs,
     if (threadIdx.x == 0) sums[c] = leaf[0];
 }
 
+// The same per-chunk sums when every 128-element leaf lies inside one row of
+// the view (innermost extent a multiple of 128 -- every power-of-two grid):
+// 8 threads per leaf, thread j summing elements j, j+8, ..., j+120 straight
+// from global memory in pw_leaf's accumulator order, the 8 accumulators
+// combined by xor-shuffles in pw_leaf's ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+// order, then the chunk's leaf tree as in k_chunk_sums_tree -- bitwise, with
+// no shared-memory staging of the chunk.
+__global__ void __launch_bounds__(512) k_chunk_sums_leaf(const double* v, S3 vs, int dim, int e1,
+                                                         int e2, long B, int nleaves,
+                                                         double* sums) {
+    __shared__ double leaf[CH_MAXLEAVES];
+    const long c = blockIdx.x;
+    const int lf = threadIdx.x >> 3, j = threadIdx.x & 7;
+    const int ne = dim == 3 ? e2 : e1;
+    const long q0 = c * B + (long)lf * CH_LEAF;
+    const long row = q0 / ne;
+    const long col = q0 - row * ne;
+    const long base = dim == 3 ? (row / e1) * vs.s[0] + (row % e1) * vs.s[1] + col * vs.s[2]
+                               : row * vs.s[0] + col * vs.s[1];
+    const long st = dim == 3 ? vs.s[2] : vs.s[1];
+    double x[CH_LEAF / 8];
+#pragma unroll
+    for (int i = 0; i < CH_LEAF / 8; ++i) x[i] = v[base + (long)(8 * i + j) * st];
+    double r = x[0];
+#pragma unroll
+    for (int i = 1; i < CH_LEAF / 8; ++i) r = ad(r, x[i]);
+    const unsigned m = blockDim.x >= 32 ? 0xffffffffu : (1u << blockDim.x) - 1u;
+    r = ad(r, __shfl_xor_sync(m, r, 1));
+    r = ad(r, __shfl_xor_sync(m, r, 2));
+    r = ad(r, __shfl_xor_sync(m, r, 4));
+    if (j == 0) leaf[lf] = r;
+    __syncthreads();
+    for (int w = 1; w < nleaves; w <<= 1) {
+        const int i = threadIdx.x * 2 * w;
+        if (i + w < nleaves) leaf[i] = ad(leaf[i], leaf[i + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[c] = leaf[0];
+}
+
 // np.sum(vals * vals) of an interior view (PKG/grid.py:249): numpy squares
 // into a contiguous temporary and runs ONE flat pairwise sum over it.  The
 // split tree (n2 = n/2 rounded down to a multiple of 8, leaves <= 128) is
@@ -1112,7 +1152,11 @@ int fasmg_view_chunk_sums(const double* v, const long* vs, int dim, const int* e
         long l = B / CH_LEAF;
         if (l <= CH_MAXLEAVES && (l & (l - 1)) == 0) nleaves = (int)l;
     }
-    if (nch > 0 && nleaves > 0) {
+    const int ne = dim == 3 ? ext[2] : ext[1];
+    if (nch > 0 && nleaves > 0 && ne % CH_LEAF == 0) {
+        k_chunk_sums_leaf<<<(unsigned)nch, 8 * nleaves, 0, S(stream)>>>(
+            v, s, dim, ext[1], dim == 3 ? ext[2] : 1, B, nleaves, sums);
+    } else if (nch > 0 && nleaves > 0) {
         const size_t shm = sizeof(double) * ((size_t)nleaves * CH_PAD + nleaves);
         static bool attr = false;
         if (!attr) {
