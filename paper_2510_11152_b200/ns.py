@@ -145,6 +145,9 @@ class ProjectionStepper:
         view = lambda q: self._scratch[: int(np.prod(shapes[q]))].view(shapes[q])  # noqa: E731
         self._f = {c: Field(grid, LOC_OF[c], 1, data=view(c)) for c in self.comps}
         self._mix = {}
+        self._mix_tag = {}   # mixture buffer -> (op, slots and their generations) it holds
+        self._gen = {}       # slot -> write generation
+        self._slot_of = {id(F): name for name, F in self.slots.items()}
         self._fp = Field(grid, Location.CELL, 1, data=view("p"))
         self.held = {slot: q for q, slot in self.schedule.initial}  # slot -> quantity
         self.step_count = 0
@@ -165,6 +168,7 @@ class ProjectionStepper:
     def set_state(self, vel: dict, p=None):
         """Initial u^0 (and u^{-1} = u^0 for order 2) and p^0.
         ``vel[c]`` / ``p``: interior arrays (numpy or tensors) or None for 0."""
+        self._mix_tag.clear()
         for c in self.comps:
             F = self.field_of(f"{c}_n")
             F.data.zero_()
@@ -190,11 +194,23 @@ class ProjectionStepper:
 
     # ----------------------------------------------------------- formulas
     def _mix_field(self, key, comp, op, a: Field, b: Field) -> Field:
+        """Order-2 velocity mixture (halo 2, ghosts filled) in buffer ``key``.
+        A buffer still holding the same mixture of the same slot contents
+        (no write to either slot since, tracked by _bind's generations) is
+        reused: within a step the three momentum sources ask for EXT(w)
+        three times, EXT(v) and AVG(u) twice each."""
         M = self._mix.get(key)
         if M is None:
             M = self._mix[key] = Field(self.grid, LOC_OF[comp], 2, device=self.device)
+        sa, sb_ = self._slot_of.get(id(a)), self._slot_of.get(id(b))
+        tag = None
+        if sa is not None and sb_ is not None:
+            tag = (op, sa, self._gen.get(sa, 0), sb_, self._gen.get(sb_, 0))
+            if self._mix_tag.get(key) == tag:
+                return M
         elem(op, M.interior, [a.interior, b.interior])
         fill_ghosts(M, self.bcs[comp])
+        self._mix_tag[key] = tag
         return M
 
     def momentum_rhs(self, c: str, read: dict) -> Field:
@@ -319,7 +335,10 @@ class ProjectionStepper:
             raise ValueError(f"unknown formula {st.formula}")
 
     def _bind(self, q: str, slot: str):
+        """Every write of a slot by a schedule Step ends here: bump its
+        generation (invalidates mixtures computed from it)."""
         self.held[slot] = q
+        self._gen[slot] = self._gen.get(slot, 0) + 1
 
     def divergence(self) -> float:
         """integral_divergence of the current velocity (Eqs. div2D/div3D)."""

@@ -277,6 +277,7 @@ class SlabProjectionStepper(ProjectionStepper):
         # mixtures, the pressure rhs
         self._f = {c: mk(LOC_OF[c], 1) for c in self.comps}
         self._mix = {}
+        self._gen = {}  # slot write generations (ProjectionStepper._bind)
         self._fp = mk(Location.CELL, 1)
         self.held = {slot: q for q, slot in self.schedule.initial}
         self.step_count = 0
