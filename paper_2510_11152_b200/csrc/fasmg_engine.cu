@@ -949,8 +949,10 @@ static int lvl_alloc(Engine& E, int k, int idx, size_t bytes, double** out) {
     return 0;
 }
 
+// (slab levels too: the axis-0 neighbour planes are the halo planes the
+// sweeps keep current, and the coarse writes use global indices)
 static bool resid_tma_level(const Engine& E, int k) {
-    return E.resid_tma && E.dim == 3 && E.ea < 0 && E.tma_ok[k] && !E.sharded(k);
+    return E.resid_tma && E.dim == 3 && E.ea < 0 && E.tma_ok[k];
 }
 
 // level k's coarse correction rides on its first post-smoothing half-sweep
@@ -1474,7 +1476,7 @@ static void launch_norm(Engine& E, long& cnt) {
     const Tile t = tile_of(L);
     int npart_norm = E.npart;
     {
-        if (D == 3 && E.resid_tma && E.tma_ok[0] && !E.sharded(0)) {
+        if (D == 3 && E.resid_tma && E.tma_ok[0]) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
             if (E.resid_pf)
@@ -1685,16 +1687,16 @@ static int tma_setup(Engine& E) {
 static int coarse_setup(Engine& E) {
     if (const char* v = getenv("FASMG_COARSE_MAX")) E.coarse_max = atol(v);
     if (const char* v = getenv("FASMG_COARSE_CS")) E.coarse_cs = std::max(1, std::min(16, atoi(v)));
-    // Not with slab ranks: the cluster launch needs 8 whole SMs of one GPC
-    // at once (512 threads x 128 registers each); with virtual ranks sharing
-    // a device it can starve behind peers' spin-waits (observed: 8 virtual
-    // ranks at 512^3).  Sharded engines keep per-level launches.
+    // Slab engines run it on their replicated coarse levels (k0 >= kg: no
+    // exchange inside).  (Round 1 kept slab engines off it after 8 virtual
+    // ranks at 512^3 hung; the cause was lazy module loading during a capture
+    // -- fixed by fasmg_engine_prepare -- not the cluster launch.)
     // Edge fields keep per-level launches: the same scheme with the edge
     // transfers' phases (residual, pads, two restrictions, pad fill, pinit,
     // correction, prolongation; all bitwise) measured SLOWER than the
     // launches it replaced (EDGE_NS 512^3 V-cycle 8.26 -> 8.41 ms: ~16
     // cluster-barrier phases per level against ~2.5 us per graph launch).
-    if (E.ea >= 0 || E.coarse_max <= 0 || E.masks.size() > 16 || E.nranks > 1) return 0;
+    if (E.ea >= 0 || E.coarse_max <= 0 || E.masks.size() > 16) return 0;
     int k0 = E.nl;
     while (k0 > 0 && !E.sharded(k0 - 1) && E.L[k0 - 1].nblk <= E.coarse_max) --k0;
     if (k0 >= E.nl) return 0;
