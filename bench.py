@@ -832,8 +832,8 @@ def ns_slab_arm(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (cavity from rest)", "config": ns_config(n, world),
             "slab": {"ranks": world, "planes_per_rank": n // world,
-                     "exchange": "row blocks over torch.distributed (NCCL) + solver halos by "
-                                 "peer stores from the sweep kernels",
+                     "exchange": "row blocks over torch.distributed (%s) + solver halos by "
+                                 "peer stores from the sweep kernels" % ("gloo" if shared else "NCCL"),
                      "ranks_share_device": shared},
             "vcycles_per_step": cyc,
             "e2e": {"value": 1e3 / e2e_ms, "unit": "steps/s",

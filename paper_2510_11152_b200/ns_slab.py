@@ -87,14 +87,24 @@ class SlabField:
     """The local slabs (one per rank of this process) of one field; the
     same location / halo / dirty-flag vocabulary as grid.Field."""
 
-    def __init__(self, geom: SlabGeom, location: Location, halo: int, ranks, device):
+    def __init__(self, geom: SlabGeom, location: Location, halo: int, ranks, device,
+                 storage: dict | None = None):
+        """``storage``: optional {rank: flat float64 tensor} the parts are
+        views of (scratch fields that are never live together share one)."""
         self.geom, self.location, self.halo = geom, location, halo
-        g = geom.grid
-        ea = location.edge_axis
-        shape = [geom.m0 + 2 * halo] + [(n + 1 + 2 * (halo - 1)) if a == ea else (n + 2 * halo)
-                                         for a, n in enumerate(g.shape) if a > 0]
-        self.parts = {r: torch.zeros(shape, dtype=torch.float64, device=device) for r in ranks}
+        shape = self.part_shape(geom, location, halo)
+        if storage is None:
+            self.parts = {r: torch.zeros(shape, dtype=torch.float64, device=device) for r in ranks}
+        else:
+            n = math.prod(shape)
+            self.parts = {r: storage[r][:n].view(shape) for r in ranks}
         self.ghosts_fresh = False
+
+    @staticmethod
+    def part_shape(geom: SlabGeom, location: Location, halo: int) -> list:
+        ea = location.edge_axis
+        return [geom.m0 + 2 * halo] + [(n + 1 + 2 * (halo - 1)) if a == ea else (n + 2 * halo)
+                                       for a, n in enumerate(geom.grid.shape) if a > 0]
 
     def interior_shape(self, r):
         g, ea = self.geom.grid, self.location.edge_axis
@@ -273,12 +283,19 @@ class SlabProjectionStepper(ProjectionStepper):
         for name in self.schedule.resident_slots():
             comp = name.split("_")[0].lower()
             self.slots[name] = mk(Location.CELL, 1) if comp == "p" else mk(LOC_OF[comp], 2)
-        # transient scratch: one source buffer per component, the halo-2
-        # mixtures, the pressure rhs
-        self._f = {c: mk(LOC_OF[c], 1) for c in self.comps}
+        # transient scratch: the momentum sources and the pressure rhs are
+        # never live together (rhs_c -> solve_c per component, then the
+        # pressure solve; ns.ProjectionStepper): one buffer per rank backs
+        # them all; the halo-2 mixtures are separate
+        locs = [LOC_OF[c] for c in self.comps] + [Location.CELL]
+        numel = max(math.prod(SlabField.part_shape(self.geom, loc, 1)) for loc in locs)
+        store = {r: torch.zeros(numel, dtype=torch.float64, device=self.device)
+                 for r in ranks.ranks}
+        self._f = {c: SlabField(self.geom, LOC_OF[c], 1, ranks.ranks, self.device, store)
+                   for c in self.comps}
         self._mix = {}
         self._gen = {}  # slot write generations (ProjectionStepper._bind)
-        self._fp = mk(Location.CELL, 1)
+        self._fp = SlabField(self.geom, Location.CELL, 1, ranks.ranks, self.device, store)
         self.held = {slot: q for q, slot in self.schedule.initial}
         self.step_count = 0
         self.timing = None
