@@ -677,7 +677,17 @@ __global__ void __launch_bounds__(TPB, 4) k_correct_edge_fast(double* __restrict
 __global__ void k_final_sum(const double* __restrict__ part, int n, double* out) {
     __shared__ double sh[1024];
     double acc = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) acc = ad(acc, part[i]);
+    // the same order as one load per iteration, with 8 loads in flight
+    const int step = blockDim.x;
+    int i = threadIdx.x;
+    for (; i + 7 * step < n; i += 8 * step) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = part[i + u * step];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = ad(acc, x[u]);
+    }
+    for (; i < n; i += step) acc = ad(acc, part[i]);
     sh[threadIdx.x] = acc;
     __syncthreads();
     for (int s = blockDim.x / 2; s > 0; s >>= 1) {

@@ -9,11 +9,12 @@ from torch.profiler import ProfilerActivity, profile
 import paper_2510_11152_b200 as P
 n = int(sys.argv[1]); loc = {"cell": "CELL", "ew": "EDGE_EW", "ns": "EDGE_NS", "tb": "EDGE_TB"}[sys.argv[2]]
 cyc = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-g = P.unit_grid((n,) * 3); L = getattr(P.Location, loc)
+dim = int(os.environ.get("PROF_DIM", "3"))
+g = P.unit_grid((n,) * dim); L = getattr(P.Location, loc)
 p = P.Field(g, L); f = P.Field(g, L)
 p.interior = torch.rand(p.interior.shape, dtype=torch.float64, device="cuda")
-S = P.FasSolver(P.make_hierarchy(g, int(np.log2(n)) - 1), L, P.BoundaryCondition.dirichlet(3),
-                P.make_plan("x", 3), P.OperatorCoeffs(1.0, 1.0 if loc == "CELL" else 0.05))
+S = P.FasSolver(P.make_hierarchy(g, int(np.log2(n)) - 1), L, P.BoundaryCondition.dirichlet(dim),
+                P.make_plan("x", dim), P.OperatorCoeffs(1.0, 1.0 if loc == "CELL" else 0.05))
 e = S.engine(2, p.device); e.load(p, f); e.run(2, True)
 torch.cuda.synchronize()
 st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
