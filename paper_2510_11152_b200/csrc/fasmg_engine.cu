@@ -891,8 +891,9 @@ struct Engine {
     BcSpec bc, bch;
     std::vector<unsigned> masks;  // per smoothing step, class masks in order
     cudaStream_t stream = nullptr;
-    cudaGraph_t graph_v = nullptr, graph_vn = nullptr;
-    cudaGraphExec_t exec_v = nullptr, exec_vn = nullptr;
+    // V-cycle graphs [starts from a pending speculative half-sweep][with norm]
+    cudaGraph_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    cudaGraphExec_t execs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     long kernels_per_vcycle = 0;
     long kernels_per_vcycle_norm = 0;
     // 0: thread per block, 1: per (block, class), 2: 2.5D register march,
@@ -924,6 +925,14 @@ struct Engine {
     CUtensorMap mapF[32], mapT[32];
     int resid_tma = 1;                  // FASMG_RESID_TMA: tau / norm on the TMA march
     int corr_fuse = 1;                  // FASMG_CORR_FUSE: correction fused into the first post half-sweep
+    // ---- the next V-cycle's first half-sweep folded into the outer norm ----
+    int spec = 1;                       // FASMG_SPEC (0: off)
+    bool spec_ok = false;               // 3D cell unsharded TMA finest level, X plan, no periodic face
+    bool spec_pending = false;          // P2 holds X_new of the next V-cycle's first half-sweep
+    bool cap_pending = false, cap_spec = false;  // the variant being captured / launched
+    bool opp_p2 = false;                // this launch reads the opposite classes from P2
+    double* P2 = nullptr;               // finest level, speculative X classes (+ their pads)
+    CUtensorMap mapT2;                  // P2 boxes 36 x 10
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
     int edge_tau = 1;                   // FASMG_EDGE_TAU: edge-field tau pass in one march (k_tau_edge_tma)
     int resid_pf = 1;                   // FASMG_RESID_PF: tau/norm marches load f and the axis-0 plane a step ahead
@@ -1097,7 +1106,8 @@ static bool sweep_one(Engine& E, int k, const Tile& t) {
         const int chunk = E.march_chunk > 0 ? E.march_chunk : 4;
         dim3 blk(TX, TY, 1);
         dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
-        k_sweep_tma<EA, M><<<grd, blk, SMEM, E.stream>>>(E.mapT[k], E.mapF[k], E.P[k], L, E.bc,
+        k_sweep_tma<EA, M><<<grd, blk, SMEM, E.stream>>>(E.opp_p2 && k == 0 ? E.mapT2 : E.mapT[k],
+                                                         E.mapF[k], E.P[k], L, E.bc,
                                                          chunk, nullptr, nullptr, Lvl(), ph);
         return fused;
     }
@@ -1318,11 +1328,18 @@ static void launch_sweep_corr(Engine& E, int k, unsigned m) {
             E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc);
 }
 
+// spec_start: the previous outer norm already ran this stage's first
+// launch into P2 (k_resid_tma<2>): skip it, and let the second launch read
+// its opposite classes from P2
 template <int D>
-static void launch_smooth(Engine& E, int k, long& cnt, bool first_corr = false) {
+static void launch_smooth(Engine& E, int k, long& cnt, bool first_corr = false,
+                          bool spec_start = false) {
     const Tile t = tile_of(E.L[k]);
     for (int it = 0; it < E.s; ++it)
-        for (unsigned m : E.masks) {
+        for (int jm = 0; jm < (int)E.masks.size(); ++jm) {
+            const unsigned m = E.masks[jm];
+            if (spec_start && it == 0 && jm == 0) continue;
+            E.opp_p2 = spec_start && it == 0 && jm == 1;
             bool pushed = false;
             if (first_corr && it == 0 && m == E.masks[0]) {
                 launch_sweep_corr(E, k, m);
@@ -1330,6 +1347,7 @@ static void launch_smooth(Engine& E, int k, long& cnt, bool first_corr = false) 
             } else {
                 EA_DISPATCH(D, E.ea, (pushed = sweep_mask<D, EA>(E, k, m, t)));
             }
+            E.opp_p2 = false;
             ++cnt;
             halo_exchange<D>(E, k, m, cnt, pushed);
         }
@@ -1366,7 +1384,7 @@ static void launch_vcycle(Engine& E, long& cnt) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L), tc = tile_of(Lc);
-        launch_smooth<D>(E, k, cnt);
+        launch_smooth<D>(E, k, cnt, false, D == 3 && k == 0 && E.cap_pending);
         if (E.ea < 0) {
             {
                 if (D == 3 && resid_tma_level(E, k)) {
@@ -1485,7 +1503,20 @@ static void launch_norm(Engine& E, long& cnt) {
     const Lvl& L = E.L[0];
     const Tile t = tile_of(L);
     int npart_norm = E.npart;
-    {
+    if (D == 3 && E.cap_spec) {  // norm + the next V-cycle's first half-sweep (into P2)
+        const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+        const dim3 g = resid_grid(L, ch), b(rsw::TX, rsw::TY, 1);
+        if (E.masks[0] == 0x96u)
+            k_resid_tma<2, -1, true, 0x96u><<<g, b, E.norm_smem, E.stream>>>(
+                E.mapT[0], E.P[0], E.F[0], L, E.bc, ch, E.part, nullptr, nullptr, L, nullptr,
+                E.P2, E.P[0]);
+        else
+            k_resid_tma<2, -1, true, 0x69u><<<g, b, E.norm_smem, E.stream>>>(
+                E.mapT[0], E.P[0], E.F[0], L, E.bc, ch, E.part, nullptr, nullptr, L, nullptr,
+                E.P2, E.P[0]);
+        npart_norm = (int)(g.x * g.y * g.z);
+        ++cnt;
+    } else {
         if (D == 3 && E.resid_tma && E.tma_ok[0]) {
             const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
             const dim3 g = resid_grid(L, ch);
@@ -1535,8 +1566,11 @@ static void launch_norm(Engine& E, long& cnt) {
     }
 }
 
+// capture the V-cycle (+ norm) variant for the current speculation state
 static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* ex) {
     long cnt = 0;
+    E.cap_pending = E.spec_ok && E.spec_pending;
+    E.cap_spec = E.spec_ok && with_norm;
     cudaError_t e = cudaStreamBeginCapture(E.stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return fasmg_check(e);
     if (E.dim == 3) {
@@ -1553,9 +1587,29 @@ static int capture(Engine& E, bool with_norm, cudaGraph_t* g, cudaGraphExec_t* e
     if (e != cudaSuccess) return fasmg_check(e);
     e = cudaGraphInstantiate(ex, *g, 0);
     if (e != cudaSuccess) return fasmg_check(e);
-    if (with_norm) E.kernels_per_vcycle_norm = cnt;
-    else E.kernels_per_vcycle = cnt;
+    if (!E.cap_pending) {
+        if (with_norm) E.kernels_per_vcycle_norm = cnt;
+        else E.kernels_per_vcycle = cnt;
+    }
+    E.cap_pending = E.cap_spec = false;
     return 0;
+}
+
+// the graph variant for the current state, and the state after it runs
+static void graph_slot(Engine& E, bool with_norm, cudaGraph_t** g, cudaGraphExec_t** ex) {
+    const int pi = E.spec_ok && E.spec_pending ? 1 : 0;
+    *g = &E.graphs[pi][with_norm ? 1 : 0];
+    *ex = &E.execs[pi][with_norm ? 1 : 0];
+}
+static void after_launch(Engine& E, bool with_norm) { E.spec_pending = E.spec_ok && with_norm; }
+
+// leave speculation: P's interior already is the state; rebuild the pads
+// the speculative norm overwrote (ghosts of X_new) from it
+static void spec_cancel(Engine& E) {
+    if (!E.spec_pending) return;
+    long cnt = 0;
+    launch_pad_fill<3>(E, 0, cnt);
+    E.spec_pending = false;
 }
 
 // Tensor maps of a level's blocked array as a 4D tensor (pitch, E1, E0,
@@ -1628,6 +1682,35 @@ static int tma2d_attr() {
     return fasmg_check(e);
 }
 
+// The outer norm also runs the next V-cycle's first pre-smoothing half-
+// sweep into P2 (k_resid_tma<2>): 3D cell-centred unsharded TMA finest
+// level, the norm on the TMA march, an X plan (first two launches the two
+// complementary parity groups) and no periodic face (a periodic ghost is
+// written by the opposite side's thread).
+static int spec_setup(Engine& E) {
+    if (const char* v = getenv("FASMG_SPEC")) E.spec = atoi(v);
+    if (!E.spec || E.dim != 3 || E.ea >= 0 || E.nranks > 1 || !E.tma_ok[0] || !E.resid_tma ||
+        E.masks.size() < 2 || E.nl < 2)
+        return 0;
+    const unsigned m0 = E.masks[0];
+    if (!((m0 == 0x96u || m0 == 0x69u) && E.masks[1] == (m0 ^ 0xFFu))) return 0;
+    for (int a = 0; a < 3; ++a)
+        if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return 0;
+    const Lvl& L = E.L[0];
+    const size_t bytes = sizeof(double) * (size_t)L.cls * 8;
+    if (int st = lvl_alloc(E, 0, 5, bytes, &E.P2)) return st;
+    cudaMemsetAsync(E.P2, 0, bytes, E.stream);
+    if (!encode_map(&E.mapT2, E.P2, L, tsw::HX, tsw::HY)) return 0;
+    cudaError_t e = cudaFuncSetAttribute(k_resid_tma<2, -1, true, 0x96u>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, E.norm_smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_resid_tma<2, -1, true, 0x69u>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, E.norm_smem);
+    if (e != cudaSuccess) return fasmg_check(e);
+    E.spec_ok = true;
+    return 0;
+}
+
 static int tma_setup(Engine& E) {
     if (E.sweep_variant != 4) return 0;
     long min_blocks = 1L << 21;  // FASMG_TMA_MIN: smaller levels are launch-latency bound
@@ -1681,6 +1764,7 @@ static int tma_setup(Engine& E) {
     if (!st) st = fasmg_check(cudaFuncSetAttribute(k_resid_tma<1, -1, true>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)rsw::SMEM));
+    if (!st) st = spec_setup(E);
     if (const char* v = getenv("FASMG_EDGE_TAU")) E.edge_tau = atoi(v);
     if (const char* v = getenv("FASMG_RESID_PF")) E.resid_pf = atoi(v);
     if (const char* v = getenv("FASMG_ETAU_CHUNK")) E.etau_chunk = std::max(1, atoi(v));
@@ -2036,10 +2120,11 @@ void fasmg_engine_destroy(void* h) {
     Engine* E = (Engine*)h;
     if (!E) return;
     cudaStreamSynchronize(E->stream);
-    if (E->exec_v) cudaGraphExecDestroy(E->exec_v);
-    if (E->exec_vn) cudaGraphExecDestroy(E->exec_vn);
-    if (E->graph_v) cudaGraphDestroy(E->graph_v);
-    if (E->graph_vn) cudaGraphDestroy(E->graph_vn);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            if (E->execs[a][b]) cudaGraphExecDestroy(E->execs[a][b]);
+            if (E->graphs[a][b]) cudaGraphDestroy(E->graphs[a][b]);
+        }
     for (void* ptr : E->owned) cudaFree(ptr);
     if (E->arena) {
         if (E->arena->last == E) E->arena->last = nullptr;
@@ -2059,6 +2144,7 @@ void fasmg_engine_destroy(void* h) {
 int fasmg_engine_load(void* h, const double* pcore, const long* ps, const double* fcore,
                       const long* fs) {
     Engine* E = (Engine*)h;
+    E->spec_pending = false;  // new state: P2 no longer describes it
     if (E->arena && E->arena->last != E) {  // another engine used the arrays: start fresh
         // (the finest P and F are skipped: the pack below writes their whole
         // core box, pads included, before anything reads them)
@@ -2122,12 +2208,15 @@ int fasmg_engine_run(void* h, int count, int with_norm, double* sumsq, int use_g
     int st;
     for (int it = 0; it < count; ++it) {
         if (use_graph) {
-            cudaGraphExec_t* ex = with_norm ? &E->exec_vn : &E->exec_v;
-            cudaGraph_t* g = with_norm ? &E->graph_vn : &E->graph_v;
+            cudaGraphExec_t* ex;
+            cudaGraph_t* g;
+            graph_slot(*E, with_norm != 0, &g, &ex);
             if (!*ex && (st = capture(*E, with_norm != 0, g, ex))) return st;
             if ((st = fasmg_check(cudaGraphLaunch(*ex, E->stream)))) return st;
         } else {
             long cnt = 0;
+            E->cap_pending = E->spec_ok && E->spec_pending;
+            E->cap_spec = E->spec_ok && with_norm;
             if (E->dim == 3) {
                 launch_vcycle<3>(*E, cnt);
                 if (with_norm) launch_norm<3>(*E, cnt);
@@ -2135,11 +2224,13 @@ int fasmg_engine_run(void* h, int count, int with_norm, double* sumsq, int use_g
                 launch_vcycle<2>(*E, cnt);
                 if (with_norm) launch_norm<2>(*E, cnt);
             }
+            E->cap_pending = E->cap_spec = false;
             if (with_norm)
                 cudaMemcpyAsync(E->hsum, E->dsum, sizeof(double), cudaMemcpyDeviceToHost,
                                 E->stream);
             if ((st = fasmg_check_launch())) return st;
         }
+        after_launch(*E, with_norm != 0);
     }
     if (with_norm) {
         if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
@@ -2155,10 +2246,12 @@ int fasmg_engine_launch(void* h, int count, int with_norm) {
     Engine* E = (Engine*)h;
     int st;
     for (int it = 0; it < count; ++it) {
-        cudaGraphExec_t* ex = with_norm ? &E->exec_vn : &E->exec_v;
-        cudaGraph_t* g = with_norm ? &E->graph_vn : &E->graph_v;
+        cudaGraphExec_t* ex;
+        cudaGraph_t* g;
+        graph_slot(*E, with_norm != 0, &g, &ex);
         if (!*ex && (st = capture(*E, with_norm != 0, g, ex))) return st;
         if ((st = fasmg_check(cudaGraphLaunch(*ex, E->stream)))) return st;
+        after_launch(*E, with_norm != 0);
     }
     return 0;
 }
@@ -2172,8 +2265,9 @@ int fasmg_engine_launch(void* h, int count, int with_norm) {
 // capturing deadlocks until k_wait's guard traps.
 int fasmg_engine_prepare(void* h, int with_norm) {
     Engine* E = (Engine*)h;
-    cudaGraphExec_t* ex = with_norm ? &E->exec_vn : &E->exec_v;
-    cudaGraph_t* g = with_norm ? &E->graph_vn : &E->graph_v;
+    cudaGraphExec_t* ex;
+    cudaGraph_t* g;
+    graph_slot(*E, with_norm != 0, &g, &ex);
     if (!*ex) return capture(*E, with_norm != 0, g, ex);
     return 0;
 }
@@ -2198,6 +2292,7 @@ int fasmg_engine_level_geom(void* h, int k, long* out) {
 
 int fasmg_engine_level_copy(void* h, int k, int which, double* dst) {
     Engine* E = (Engine*)h;
+    spec_cancel(*E);
     if (k < 0 || k >= E->nl) return fasmg_set_error(FASMG_EINVAL, "level out of range");
     const double* src = which == 0 ? E->P[k] : (which == 1 ? E->F[k] : nullptr);
     if (!src) return fasmg_set_error(FASMG_EINVAL, "no such array");
@@ -2210,6 +2305,7 @@ int fasmg_engine_level_copy(void* h, int k, int which, double* dst) {
 // Residual sum of squares of the current finest state (no V-cycle).
 int fasmg_engine_residual_sumsq(void* h, double* sumsq) {
     Engine* E = (Engine*)h;
+    spec_cancel(*E);
     long cnt = 0;
     if (E->dim == 3) launch_norm<3>(*E, cnt);
     else launch_norm<2>(*E, cnt);
@@ -2225,6 +2321,7 @@ int fasmg_engine_residual_sumsq(void* h, double* sumsq) {
 // timing bench.py reports for the roofline.
 int fasmg_engine_time_sweeps(void* h, int k, int reps, double* ms) {
     Engine* E = (Engine*)h;
+    spec_cancel(*E);
     if (k < 0 || k >= E->nl || reps < 1) return fasmg_set_error(FASMG_EINVAL, "bad level/reps");
     cudaEvent_t a, b;
     int st = fasmg_check(cudaEventCreate(&a));

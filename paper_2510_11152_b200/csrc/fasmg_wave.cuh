@@ -317,7 +317,19 @@ constexpr size_t SMEM = 2 * SLOT * 8 + 2 * 8;
 constexpr unsigned TXB = 8u * HX * (TY + 2) * 8u;
 }  // namespace rsw
 
-template <int MODE, int EA = -1, bool RESID_PF = false>
+// MODE 2 (cell fields): the outer norm of MODE 0 AND, from the same loaded
+// values, the NEXT V-cycle's first pre-smoothing half-sweep of the classes
+// in MX (speculative: the host decides afterwards whether that cycle runs).
+// A half-sweep reads exactly what the residual reads -- the opposite
+// classes around the point (box + axis-0 neighbour), f, in the same
+// ((((E+W)+N)+S)+T)+B order -- so X_new = (h2*f + b*ns)/denom costs no extra
+// load.  X_new goes to P2 (P keeps the state the norm describes), with the
+// ghosts the next half-sweep reads: ghost(Y_old) into P2's X-class pads;
+// ghost(X_new) into P's Y-class pads (read only by the third half-sweep;
+// a stop before it rebuilds P's pads, fasmg_engine spec_cancel).  The only
+// reader of a pad slot written here is the thread that writes it, and it
+// read the slot first.
+template <int MODE, int EA = -1, bool RESID_PF = false, unsigned MX = 0u>
 __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUtensorMap mapH,
                                                    const double* __restrict__ P,
                                                    const double* __restrict__ F, Lvl L,
@@ -325,7 +337,10 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                                                    double* __restrict__ part,
                                                    double* __restrict__ Pc,
                                                    double* __restrict__ Fc, Lvl Lc,
-                                                   double* __restrict__ PIc) {
+                                                   double* __restrict__ PIc,
+                                                   double* __restrict__ P2 = nullptr,
+                                                   double* Pw = nullptr) {
+    static_assert(MODE != 2 || (EA == -1 && MX != 0u), "MODE 2: cell fields, a class mask");
     using namespace rsw;
     extern __shared__ __align__(128) double sm[];
     unsigned long long* bar = (unsigned long long*)(sm + 2 * SLOT);
@@ -375,6 +390,7 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
 #pragma unroll
             for (int c = 0; c < 8; ++c) pc[c] = S[c * HB + ci];
             double rp = 0.0, rr = 0.0;
+            double xn[8];  // (MODE 2) numerators of the speculative half-sweep
 #pragma unroll
             for (int c = 7; c >= 0; --c) {
                 double ns = 0.0;
@@ -395,13 +411,29 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
                 }
                 const double lap = ml(sb(ns, ml(6.0, pc[c])), L.inv_h2);
                 const double r = sb(fv[c], sb(ml(L.a, pc[c]), ml(L.b, lap)));
-                if (MODE == 0) {
+                if (MODE == 2 && ((MX >> c) & 1u)) xn[c] = ad(ml(L.h2, fv[c]), ml(L.b, ns));
+                if (MODE == 0 || MODE == 2) {
                     // edge fields: wall points are not unknowns (PKG/grid.py:199-208)
                     int bw[3] = {b0, b1, b2};
                     if (!is_wall<3, EA>(L, c, bw)) acc = ad(acc, ml(r, r));
                 } else {
                     if (c == 7) { rp = pc[c]; rr = r; }
                     else { rp = ad(rp, pc[c]); rr = ad(rr, r); }
+                }
+            }
+            if (MODE == 2) {
+                int bb[3] = {b0, b1, b2};
+                const bool bnd = on_boundary<3>(L, bb);
+                const long o = at<3>(L, 0, b0, b1, b2);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if ((MX >> c) & 1u) {
+                        const double v = dvr(xn[c], L.denom, L.rden);
+                        P2[o + (long)c * L.cls] = v;
+                        if (bnd) write_pads<3, -1>(Pw, L, bc, c, bb, o + (long)c * L.cls, v);
+                    } else if (bnd) {
+                        write_pads<3, -1>(P2, L, bc, c, bb, o + (long)c * L.cls, pc[c]);
+                    }
                 }
             }
             if (MODE == 1) {
@@ -418,7 +450,7 @@ __global__ void __launch_bounds__(256) k_resid_tma(const __grid_constant__ CUten
         if (RESID_PF && b0 < b0e) load_tile(b0 + 1);
         __syncthreads();  // slot s is refilled by the next step's prefetch
     }
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 2) {
         double* red = sm;  // the ring is free now
         red[tid] = acc;
         __syncthreads();

@@ -203,3 +203,75 @@ def test_edge_tau_march_vs_oracle(P, monkeypatch, shape, loc, spec, env):
     assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
     off, _ = run_gpu(P, monkeypatch, {**e, "FASMG_EDGE_TAU": 0}, shape, loc, faces, p0, f0, ml, 2)
     assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
+
+
+@pytest.mark.parametrize("shape,spec,env,a", [
+    ((64, 64, 64), "dirichlet", {}, 1.0),
+    ((48, 112, 80), "mixed_dn", {}, 1.0),                       # partial tiles, Neumann faces
+    ((96, 64, 128), "mixed_dn", {"FASMG_MARCH_CHUNK": 5}, 1.0),  # ragged chunks
+    ((64, 64, 64), "neumann", {}, 0.0),                          # singular (pressure-like)
+    ((64, 64, 64), "lid", {"FASMG_CORR_FUSE": 0}, 1.0),
+])
+def test_speculative_first_sweep_vs_oracle(P, monkeypatch, shape, spec, env, a):
+    """The outer norm also running the next V-cycle's first pre-smoothing
+    half-sweep into a second buffer (k_resid_tma<2>, FASMG_SPEC), forced onto
+    small levels over 4 V-cycles: fields bitwise equal to the oracle and to
+    FASMG_SPEC=0, residual histories within 1e-10 / identical."""
+    import oracle as O
+    faces = faces_of(spec) if spec in FACES else C.bc_faces(3, spec)
+    ml = 3
+    p0 = C.rand_field(93, shape, "cell", 1)
+    f0 = C.rand_field(94, shape, "cell", 1)
+    op = O.OField(shape, "cell", 1, p0.copy())
+    of = O.OField(shape, "cell", 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, a, 0.5, faces, O.plan_colors("x", 3), 1e-30, 4, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    e = {"FASMG_TMA_MIN": 0, **env}
+    got, rep = run_gpu_a(P, monkeypatch, e, shape, faces, p0, f0, ml, 4, a)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+    off, rep2 = run_gpu_a(P, monkeypatch, {**e, "FASMG_SPEC": 0}, shape, faces, p0, f0, ml, 4, a)
+    assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
+    assert rep.residual_history == rep2.residual_history
+
+
+def test_speculation_state_transitions(P, monkeypatch):
+    """Engine calls that read or replace the state while a speculative
+    half-sweep is pending (store, the bare V-cycle, level copies, the
+    residual, a new load) see exactly the non-speculative engine's values."""
+    import ctypes
+    from paper_2510_11152_b200 import _native as N
+    monkeypatch.setenv("FASMG_TMA_MIN", "0")
+    shape = (64, 64, 64)
+    g = P.unit_grid(shape)
+    p0 = C.rand_field(95, shape, "cell", 1)
+    f0 = C.rand_field(96, shape, "cell", 1)
+    outs = []
+    for spec in ("1", "0"):
+        monkeypatch.setenv("FASMG_SPEC", spec)
+        S = P.FasSolver(P.make_hierarchy(g, 3), P.Location.CELL, P.BoundaryCondition.dirichlet(3),
+                        P.make_plan("x", 3), P.OperatorCoeffs(1.0, 0.5))
+        p = P.Field(g, P.Location.CELL, 1, p0.copy())
+        f = P.Field(g, P.Location.CELL, 1, f0.copy())
+        e = S.engine(2, p.device)
+        e.load(p, f)
+        r = [e.run(1, True), e.run(1, True)]
+        e.store(p)                       # pending: the stored state is the real one
+        rs = ctypes.c_double()
+        N.call("fasmg_engine_residual_sumsq", e.handle, ctypes.byref(rs))  # cancels
+        r.append(rs.value)
+        r.append(e.run(2, True))
+        e.run(1, False)                  # bare V-cycle after a pending norm
+        r.append(e.run(1, True))
+        q = P.Field(g, P.Location.CELL, 1, p0.copy())
+        e.store(q)
+        e.load(q, f)                     # a new load drops the speculation
+        r.append(e.run(1, True))
+        e.store(q)
+        torch.cuda.synchronize()
+        outs.append((p.data.cpu().numpy(), q.data.cpu().numpy(), r))
+    assert np.array_equal(outs[0][0].view(np.uint64), outs[1][0].view(np.uint64))
+    assert np.array_equal(outs[0][1].view(np.uint64), outs[1][1].view(np.uint64))
+    np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-13, atol=0)
