@@ -383,6 +383,10 @@ def b200_arm(args):
         eng = solver.engine(2, dev)
         eng.load(p, f)
         run_step = lambda: eng.run(1, with_norm=True)  # noqa: E731
+        scale_res = g.h ** (dim / 2.0)
+        # K outer iterations as FasSolver.solve runs them: one graph launch,
+        # the residual test on the device (tol -1: never met, so exactly K)
+        run_steps = lambda k: eng.solve_loop(k, -1.0, scale_res)  # noqa: E731
         stream_handle = eng.stream.value
         local_dof = dof
         slab_detail = None
@@ -399,6 +403,9 @@ def b200_arm(args):
         def run_step():
             eng.launch(1, True)
             return eng.result()
+
+        def run_steps(k):
+            return [run_step() for _ in range(k)]
         stream_handle = eng.stream.value
         local_dof = dof // world
         slab_detail = (f"axis-0 slabs, halo push per half-sweep over CUDA IPC/NVLink, "
@@ -410,10 +417,12 @@ def b200_arm(args):
     clocks.start()
     time.sleep(0.3)
 
-    # --- device-resident timed region: K outer iterations (V-cycle + norm,
-    #     host reads the residual each step exactly as FasSolver.solve does)
-    for _ in range(W):
-        run_step()
+    # --- device-resident timed region: K outer iterations (V-cycle + norm +
+    #     convergence test), issued the way FasSolver.solve issues them:
+    #     single GPU -> one graph launch with the test on the device
+    #     (fasmg_engine_solve); slabs -> per-iteration launch + host read
+    run_steps(1)      # builds the graph entered from a fresh load
+    run_steps(W - 1)  # ... and the one entered with a speculation pending
     st = torch.cuda.ExternalStream(stream_handle, device=dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -422,9 +431,7 @@ def b200_arm(args):
     torch.cuda.synchronize()
     t0 = time.time()
     ev0.record(st)
-    hist = []
-    for _ in range(K):
-        hist.append(run_step())
+    hist = run_steps(K)
     ev1.record(st)
     torch.cuda.synchronize()
     t1 = time.time()
@@ -433,6 +440,17 @@ def b200_arm(args):
     if dist is not None:
         dist.barrier()
     value = dof / (ms_step * 1e-3) / 1e6
+    host_loop = None
+    if world == 1:  # the per-iteration host loop (launch + read), beside it
+        torch.cuda.synchronize()
+        ev0.record(st)
+        for _ in range(K):
+            run_step()
+        ev1.record(st)
+        torch.cuda.synchronize()
+        host_loop = {"ms_per_step": ev0.elapsed_time(ev1) / K,
+                     "api": "engine.run(1, with_norm=True) per iteration: graph launch + "
+                            "host read of the norm + host-side test"}
 
     # --- live per-launch timing of the dominant kernel (finest half-sweep)
     sweep_ms = eng.time_sweeps(0, 16)
@@ -588,9 +606,15 @@ def b200_arm(args):
             "slab": slab_detail,
             "roofline": roofline, "cpu_baseline": cpu,
             "cpu_baseline_reference_1core": numba, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": kernels * K,
-            "kernels_per_step": kernels,
-            "residual_last": (g.h ** (dim / 2.0)) * float(np.sqrt(hist[-1])) if hist else None,
+            "clocks": clocks.summary(),
+            "gpu_launches": (kernels + (1 if world == 1 else 0)) * K,
+            "kernels_per_step": kernels + (1 if world == 1 else 0),
+            "solve_loop": ("one graph launch for the K iterations (conditional WHILE node, "
+                           "device-side residual test k_conv)" if world == 1 else
+                           "per-iteration launch + host read"),
+            "host_loop": host_loop,
+            "residual_last": (hist[-1] if world == 1 else
+                              (g.h ** (dim / 2.0)) * float(np.sqrt(hist[-1]))) if hist else None,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -241,6 +241,13 @@ int fasmg_engine_launch(void* engine, int count, int with_norm);
  * sharing a device is prepared before any launches (lazy module loading
  * would otherwise wait on the peers' spin-waits) */
 int fasmg_engine_prepare(void* engine, int with_norm);
+/* the whole outer solve loop (PKG/fas.py:147-154) as ONE graph launch: up to
+ * k_max V-cycles + norms on the loaded state, the convergence test
+ * res = scale*sqrt(sumsq) <= tol evaluated on the device (a WHILE
+ * conditional node); history (host, k_max doubles) and *iters out.
+ * Single-rank engines. */
+int fasmg_engine_solve(void* engine, int k_max, double tol, double scale, double* history,
+                       int* iters);
 /* self-test of the sweep kernels' reciprocal division: n random normal
  * numerators (|exponent| <= emax) x nd divisors; *bad = quotients whose bits
  * differ from IEEE division (expected 0) */

@@ -62,6 +62,7 @@ _SIGS = {
     "fasmg_engine_time_sweeps": "viiD",
     "fasmg_engine_launch": "vii",
     "fasmg_engine_prepare": "vi",
+    "fasmg_engine_solve": "viddDI",
     "fasmg_selftest_div": "llDiiL",
     "fasmg_engine_level_geom": "viL",
     "fasmg_engine_level_copy": "viip",

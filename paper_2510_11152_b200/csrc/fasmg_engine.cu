@@ -933,6 +933,13 @@ struct Engine {
     bool opp_p2 = false;                // this launch reads the opposite classes from P2
     double* P2 = nullptr;               // finest level, speculative X classes (+ their pads)
     CUtensorMap mapT2;                  // P2 boxes 36 x 10
+    // ---- the whole solve as one graph launch (device-side convergence test) ----
+    cudaGraph_t gsolve[2] = {nullptr, nullptr};        // [starts from a pending speculation]
+    cudaGraphExec_t xsolve[2] = {nullptr, nullptr};
+    double* dhist = nullptr;            // residual history (device), SOLVE_CAP entries
+    int* dit = nullptr;                 // V-cycles run (device)
+    double* dctl = nullptr;             // {tol, scale, k_max} (device)
+    double* hbuf = nullptr;             // pinned: ctl (3) + history (SOLVE_CAP) + count
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
     int edge_tau = 1;                   // FASMG_EDGE_TAU: edge-field tau pass in one march (k_tau_edge_tma)
     int resid_pf = 1;                   // FASMG_RESID_PF: tau/norm marches load f and the axis-0 plane a step ahead
@@ -1603,6 +1610,79 @@ static void graph_slot(Engine& E, bool with_norm, cudaGraph_t** g, cudaGraphExec
 }
 static void after_launch(Engine& E, bool with_norm) { E.spec_pending = E.spec_ok && with_norm; }
 
+// ---------------------------------------------------- device-side solve loop
+// FasSolver.solve's outer loop (PKG/fas.py:147-154) with the convergence test
+// on the device: after each V-cycle + norm, k_conv forms res = scale *
+// sqrt(sumsq) exactly as the host does (IEEE sqrt and multiply), appends it to
+// the history and sets the WHILE node's condition to !(res <= tol) && it <
+// k_max -- so a whole solve is ONE graph launch, with no host round trip
+// between V-cycles, and the same cycles / history / fields as the host loop.
+constexpr int SOLVE_CAP = 4096;
+__global__ void k_conv(const double* __restrict__ dsum, const double* __restrict__ ctl,
+                       double* __restrict__ hist, int* __restrict__ it,
+                       cudaGraphConditionalHandle h) {
+    const double res = ml(ctl[1], __dsqrt_rn(dsum[0]));
+    const int i = it[0];
+    hist[i] = res;
+    it[0] = i + 1;
+    cudaGraphSetConditional(h, (!(res <= ctl[0]) && (double)(i + 1) < ctl[2]) ? 1u : 0u);
+}
+
+template <int D>
+static void capture_iteration(Engine& E, bool pending, cudaGraphConditionalHandle h) {
+    long cnt = 0;
+    E.cap_pending = E.spec_ok && pending;
+    E.cap_spec = E.spec_ok;
+    launch_vcycle<D>(E, cnt);
+    launch_norm<D>(E, cnt);
+    E.cap_pending = E.cap_spec = false;
+    k_conv<<<1, 1, 0, E.stream>>>(E.dsum, E.dctl, E.dhist, E.dit, h);
+}
+
+// [first iteration (from the current speculation state)] -> WHILE(cond) {
+// iteration (from the pending state the previous one leaves) }
+static int build_solve_graph(Engine& E, int ps) {
+    cudaGraph_t g = nullptr;
+    cudaGraphConditionalHandle h;
+    int st = fasmg_check(cudaGraphCreate(&g, 0));
+    if (!st) st = fasmg_check(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+    if (!st) st = fasmg_check(cudaStreamBeginCaptureToGraph(E.stream, g, nullptr, nullptr, 0,
+                                                             cudaStreamCaptureModeThreadLocal));
+    if (st) { if (g) cudaGraphDestroy(g); return st; }
+    if (E.dim == 3) capture_iteration<3>(E, ps != 0, h);
+    else capture_iteration<2>(E, ps != 0, h);
+    // the WHILE node after the first iteration's k_conv
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    st = fasmg_check(cudaStreamGetCaptureInfo(E.stream, &cs, nullptr, nullptr, &deps, &ndeps));
+    cudaGraphNodeParams prm = {};
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    cudaGraphNode_t cond;
+    if (!st) st = fasmg_check(cudaGraphAddNode(&cond, g, deps, ndeps, &prm));
+    if (!st) st = fasmg_check(cudaStreamUpdateCaptureDependencies(E.stream, &cond, 1,
+                                                                  cudaStreamSetCaptureDependencies));
+    cudaGraph_t g2 = nullptr;
+    cudaError_t e = cudaStreamEndCapture(E.stream, &g2);
+    if (!st) st = fasmg_check(e);
+    if (st) { cudaGraphDestroy(g); return st; }
+    cudaGraph_t body = prm.conditional.phGraph_out[0];
+    st = fasmg_check(cudaStreamBeginCaptureToGraph(E.stream, body, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal));
+    if (st) { cudaGraphDestroy(g); return st; }
+    if (E.dim == 3) capture_iteration<3>(E, true, h);
+    else capture_iteration<2>(E, true, h);
+    cudaGraph_t b2 = nullptr;
+    e = cudaStreamEndCapture(E.stream, &b2);
+    if ((st = fasmg_check(e))) { cudaGraphDestroy(g); return st; }
+    if ((st = fasmg_check(cudaGraphInstantiate(&E.xsolve[ps], g, 0)))) { cudaGraphDestroy(g); return st; }
+    E.gsolve[ps] = g;
+    return 0;
+}
+
 // leave speculation: P's interior already is the state; rebuild the pads
 // the speculative norm overwrote (ghosts of X_new) from it
 static void spec_cancel(Engine& E) {
@@ -2120,11 +2200,18 @@ void fasmg_engine_destroy(void* h) {
     Engine* E = (Engine*)h;
     if (!E) return;
     cudaStreamSynchronize(E->stream);
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < 2; ++a) {
         for (int b = 0; b < 2; ++b) {
             if (E->execs[a][b]) cudaGraphExecDestroy(E->execs[a][b]);
             if (E->graphs[a][b]) cudaGraphDestroy(E->graphs[a][b]);
         }
+        if (E->xsolve[a]) cudaGraphExecDestroy(E->xsolve[a]);
+        if (E->gsolve[a]) cudaGraphDestroy(E->gsolve[a]);
+    }
+    if (E->dhist) cudaFree(E->dhist);
+    if (E->dit) cudaFree(E->dit);
+    if (E->dctl) cudaFree(E->dctl);
+    if (E->hbuf) cudaFreeHost(E->hbuf);
     for (void* ptr : E->owned) cudaFree(ptr);
     if (E->arena) {
         if (E->arena->last == E) E->arena->last = nullptr;
@@ -2269,6 +2356,41 @@ int fasmg_engine_prepare(void* h, int with_norm) {
     cudaGraph_t* g;
     graph_slot(*E, with_norm != 0, &g, &ex);
     if (!*ex) return capture(*E, with_norm != 0, g, ex);
+    return 0;
+}
+
+// A whole outer solve loop (PKG/fas.py:147-154) as one graph launch: up to
+// k_max V-cycles + norms on the loaded state, stopping on the device at the
+// first res = scale*sqrt(sumsq) <= tol.  history: host array of k_max doubles;
+// *iters = V-cycles run.  Single-rank engines (slab ranks loop on the host).
+int fasmg_engine_solve(void* h, int k_max, double tol, double scale, double* history,
+                       int* iters) {
+    Engine* E = (Engine*)h;
+    if (E->nranks > 1) return fasmg_set_error(FASMG_EINVAL, "device solve loop: single-rank engines only");
+    if (k_max < 1 || k_max > SOLVE_CAP) return fasmg_set_error(FASMG_EINVAL, "k_max out of range");
+    int st;
+    if (!E->dhist) {
+        if ((st = fasmg_check(cudaMalloc(&E->dhist, sizeof(double) * SOLVE_CAP)))) return st;
+        if ((st = fasmg_check(cudaMalloc(&E->dit, sizeof(int))))) return st;
+        if ((st = fasmg_check(cudaMalloc(&E->dctl, sizeof(double) * 3)))) return st;
+        if ((st = fasmg_check(cudaMallocHost(&E->hbuf, sizeof(double) * (SOLVE_CAP + 4))))) return st;
+    }
+    const int ps = E->spec_ok && E->spec_pending ? 1 : 0;
+    if (!E->xsolve[ps] && (st = build_solve_graph(*E, ps))) return st;
+    E->hbuf[0] = tol;
+    E->hbuf[1] = scale;
+    E->hbuf[2] = (double)k_max;
+    if ((st = fasmg_check(cudaMemcpyAsync(E->dctl, E->hbuf, sizeof(double) * 3,
+                                          cudaMemcpyHostToDevice, E->stream)))) return st;
+    if ((st = fasmg_check(cudaMemsetAsync(E->dit, 0, sizeof(int), E->stream)))) return st;
+    if ((st = fasmg_check(cudaGraphLaunch(E->xsolve[ps], E->stream)))) return st;
+    int* hcount = (int*)(E->hbuf + SOLVE_CAP + 3);
+    cudaMemcpyAsync(hcount, E->dit, sizeof(int), cudaMemcpyDeviceToHost, E->stream);
+    cudaMemcpyAsync(E->hbuf + 3, E->dhist, sizeof(double) * k_max, cudaMemcpyDeviceToHost, E->stream);
+    if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
+    E->spec_pending = E->spec_ok;  // every iteration ended with the fused norm
+    *iters = *hcount;
+    for (int i = 0; i < *hcount; ++i) history[i] = E->hbuf[3 + i];
     return 0;
 }
 

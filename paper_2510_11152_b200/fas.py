@@ -114,6 +114,17 @@ class _Engine:
             N.call("fasmg_engine_store", self.handle, N.ptr(pc), N.strides(pc))
             N.wait(N.torch_stream(self.device), self.stream)
 
+    def solve_loop(self, k_max: int, tol: float, scale: float) -> list:
+        """Up to ``k_max`` V-cycles + norms in ONE graph launch, stopping on
+        the device at the first ``scale*sqrt(sumsq) <= tol`` (the host loop's
+        test, bitwise): the residual history."""
+        hist = (ctypes.c_double * k_max)()
+        n = ctypes.c_int(0)
+        with torch.cuda.device(self.device):
+            N.call("fasmg_engine_solve", self.handle, int(k_max), float(tol), float(scale), hist,
+                   ctypes.byref(n))
+        return list(hist[: n.value])
+
     def run(self, count: int, with_norm: bool, use_graph: bool = True) -> float:
         out = ctypes.c_double(0.0)
         with torch.cuda.device(self.device):
@@ -238,12 +249,16 @@ class FasSolver:
         g = self.hierarchy.fine
         scale = g.h ** (g.dim / 2.0)
         history: list = []
-        for _ in range(params.k_max):
-            sumsq = e.run(1, with_norm=True, use_graph=self.use_graph)
-            res = scale * math.sqrt(sumsq)
-            history.append(res)
-            if res <= params.tol:
-                break
+        if self.use_graph and 1 <= params.k_max <= 4096:
+            # the loop below, with the test on the device: one graph launch
+            history = e.solve_loop(params.k_max, params.tol, scale)
+        else:
+            for _ in range(params.k_max):
+                sumsq = e.run(1, with_norm=True, use_graph=self.use_graph)
+                res = scale * math.sqrt(sumsq)
+                history.append(res)
+                if res <= params.tol:
+                    break
         e.store(p)
         fill_ghosts(p, self.bc)
         if singular:
