@@ -941,6 +941,7 @@ struct Engine {
     double* dctl = nullptr;             // {tol, scale, k_max} (device)
     double* hbuf = nullptr;             // pinned: ctl (3) + history (SOLVE_CAP) + count
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
+    int num_sms = 148;
     int edge_tau = 1;                   // FASMG_EDGE_TAU: edge-field tau pass in one march (k_tau_edge_tma)
     int resid_pf = 1;                   // FASMG_RESID_PF: tau/norm marches load f and the axis-0 plane a step ahead
     int etau_chunk = 8;                 // FASMG_ETAU_CHUNK: its planes per CTA
@@ -987,6 +988,19 @@ static bool resid_tma_level(const Engine& E, int k) {
 static bool corr_fused(const Engine& E, int k) {
     if (!E.corr_fuse || E.dim != 3 || E.ea >= 0 || !E.tma_ok[k] || E.sharded(k) ||
         k + 1 >= E.nl || !E.PI[k + 1] || E.masks.size() < 2)
+        return false;
+    for (int a = 0; a < 3; ++a)
+        if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
+    const unsigned m0 = E.masks[0], m1 = E.masks[1];
+    return (m0 == 0x96u || m0 == 0x69u) && m1 == (m0 ^ 0xFFu);
+}
+
+// edge fields: level k's correction (prolongation of Corr) rides on the
+// first post-smoothing half-sweep (k_sweep_tma<EA, M, true>): the same plan
+// and boundary conditions as corr_fused, the edge_fast transfers
+static bool ecorr_fused(const Engine& E, int k) {
+    if (!E.corr_fuse || E.dim != 3 || E.ea < 0 || !E.edge_fast || !E.tma_ok[k] ||
+        E.sharded(k) || k + 1 >= E.nl || E.masks.size() < 2)
         return false;
     for (int a = 0; a < 3; ++a)
         if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
@@ -1318,16 +1332,36 @@ static void gather_level(Engine& E, int k, long& cnt) {
     launch_pad_fill<D>(E, k, cnt);
 }
 
+template <int A>
+static void launch_sweep_ecorr(Engine& E, int k, unsigned m, dim3 grd, dim3 blk, int chunk) {
+    using namespace tsw;
+    if (m == 0x96u)
+        k_sweep_tma<A, 0x96u, true><<<grd, blk, SMEM_ECORR, E.stream>>>(
+            E.mapT[k], E.mapF[k], E.P[k], E.L[k], E.bc, chunk, E.R[k + 1], E.F[k], E.L[k + 1]);
+    else
+        k_sweep_tma<A, 0x69u, true><<<grd, blk, SMEM_ECORR, E.stream>>>(
+            E.mapT[k], E.mapF[k], E.P[k], E.L[k], E.bc, chunk, E.R[k + 1], E.F[k], E.L[k + 1]);
+}
+
 // the first post-smoothing half-sweep of level k with the coarse correction
 // applied on the fly (k_sweep_tma<-1, M, true>; see corr_fused)
 static void launch_sweep_corr(Engine& E, int k, unsigned m) {
     using namespace tsw;
     const Lvl& L = E.L[k];
     const Lvl& Lc = E.L[k + 1];
-    const int chunk = E.corr_chunk > 0 ? E.corr_chunk : (E.march_chunk > 0 ? E.march_chunk : 4);
+    // (edge: longer chunks amortize the per-chunk prologue of the box
+    // correction, as long as the grid keeps >= 4 waves of 3 CTAs per SM)
+    int chunk = E.corr_chunk > 0 ? E.corr_chunk : (E.march_chunk > 0 ? E.march_chunk : 4);
+    if (E.ea >= 0 && E.corr_chunk <= 0) {
+        const long plane = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
+        for (int c = 16; c > 4; c >>= 1)
+            if (plane * ((L.B[0] + c - 1) / c) >= 4L * 3 * E.num_sms) { chunk = c; break; }
+    }
     dim3 blk(TX, TY, 1);
     dim3 grd((L.B[2] + TX - 1) / TX, (L.B[1] + TY - 1) / TY, (L.B[0] + chunk - 1) / chunk);
-    if (m == 0x96u)
+    if (E.ea >= 0) {  // edge: Pc = the coarse Corr array (k_corr_edge_*)
+        EA_DISPATCH(3, E.ea, (launch_sweep_ecorr<(EA < 0 ? 0 : EA)>(E, k, m, grd, blk, chunk)));
+    } else if (m == 0x96u)
         k_sweep_tma<-1, 0x96u, true><<<grd, blk, SMEM_CORR, E.stream>>>(
             E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc);
     else
@@ -1467,7 +1501,7 @@ static void launch_vcycle(Engine& E, long& cnt) {
         const Lvl& L = E.L[k];
         const Lvl& Lc = E.L[k + 1];
         const Tile t = tile_of(L);
-        const bool cf = D == 3 && corr_fused(E, k);  // correction rides on the first sweep
+        const bool cf = D == 3 && (corr_fused(E, k) || ecorr_fused(E, k));  // rides on the first sweep
         if (E.ea < 0) {
             if (!cf) {
                 k_correct_fast<D><<<t.grid, t.block, 0, E.stream>>>(E.P[k], L, E.P[k + 1], Lc,
@@ -1488,17 +1522,19 @@ static void launch_vcycle(Engine& E, long& cnt) {
                     k_corr_edge_pads<D><<<pg, TPB, 0, E.stream>>>(E.P[k + 1], E.PI[k + 1], Lc,
                                                                   E.bch, E.R[k + 1]);
                 }
-                ++cnt;
-                EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<t.grid, t.block, 0,
-                                                                   E.stream>>>(E.P[k], L,
-                                                                               E.R[k + 1], Lc)));
                 cnt += 2;
+                if (!cf) {
+                    EA_DISPATCH(D, E.ea, (k_correct_edge_fast<D, EA><<<t.grid, t.block, 0,
+                                                                       E.stream>>>(E.P[k], L,
+                                                                                   E.R[k + 1], Lc)));
+                    ++cnt;
+                }
             } else {
                 k_correct_edge<D><<<nb(L.nblk, TPB), TPB, 0, E.stream>>>(E.P[k], L, E.P[k + 1],
                                                                          E.PI[k + 1], Lc, E.bch);
                 ++cnt;
             }
-            launch_pad_fill<D>(E, k, cnt);
+            if (!cf) launch_pad_fill<D>(E, k, cnt);
         }
         halo_exchange<D>(E, k, ALL, cnt);
         launch_smooth<D>(E, k, cnt, cf);
@@ -1747,6 +1783,12 @@ static int tma_attr() {
     if (e == cudaSuccess && EA == -1)
         e = cudaFuncSetAttribute(k_sweep_tma<-1, 0x69u, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsw::SMEM_CORR);
+    if (e == cudaSuccess && EA >= 0)
+        e = cudaFuncSetAttribute(k_sweep_tma<(EA < 0 ? 0 : EA), 0x96u, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsw::SMEM_ECORR);
+    if (e == cudaSuccess && EA >= 0)
+        e = cudaFuncSetAttribute(k_sweep_tma<(EA < 0 ? 0 : EA), 0x69u, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsw::SMEM_ECORR);
     return fasmg_check(e);
 }
 
@@ -1822,6 +1864,12 @@ static int tma_setup(Engine& E) {
     if (const char* v = getenv("FASMG_RESID_TMA")) E.resid_tma = atoi(v);
     if (const char* v = getenv("FASMG_CORR_FUSE")) E.corr_fuse = atoi(v);
     if (const char* v = getenv("FASMG_CORR_CHUNK")) E.corr_chunk = atoi(v);
+    {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+            E.num_sms = n;
+    }
     // at most 3 CTAs per SM for the norm march: the EA = 1 instantiation
     // compiles to 64 registers, so 4 CTAs fit and then stall on the MIO
     // queue (ncu: mio_throttle, 553 us vs 350 us for the cell one at 3 CTAs);

@@ -71,6 +71,11 @@ constexpr int CX = TX + 2, CY = TY + 2, CB = CX * CY;  // corr tile (block ring)
 constexpr int CRING = 4;
 constexpr size_t SMEM = (size_t)(4 * RING * HB + 2 * 4 * FB) * 8 + 2 * 8;
 constexpr size_t SMEM_CORR = SMEM + (size_t)CRING * CB * 8;
+// (edge CORR) coarse Corr tiles: coarse indices y0-2..y0+9 x x0-3..x0+34
+// of one coarse plane per slot, ERING planes (c0-1..c0+3 of step c0)
+constexpr int ECX = TX + 6, ECY = TY + 4, ECP = ECX * ECY, ERING = 5;
+// (f is read straight from global in that variant: no f boxes, 4 CTAs/SM)
+constexpr size_t SMEM_ECORR = SMEM - (size_t)2 * 4 * FB * 8 + (size_t)ERING * ECP * 8;
 }  // namespace tsw
 
 // CORR: this is the FIRST post-smoothing half-sweep of the level and also
@@ -85,8 +90,20 @@ constexpr size_t SMEM_CORR = SMEM + (size_t)CRING * CB * 8;
 // ghost pads are written from the corrected values.  Because no CTA
 // modifies a B value, neighbours read consistent data (no cross-CTA race).
 // Requires: cell-centred, no periodic face, next half-sweep = the other color.
+//
+// Edge fields (EA >= 0) with CORR: the correction is the edge prolongation
+// (KER/numpy_backend.py:194-224, correct_edge_pt) of the coarse Corr array
+// (Pc = Corr: p_c - pinit with the homogenized ghost chain, k_corr_edge_*),
+// which varies inside a block, so it is applied where the data already is:
+// each opposite-class halo box is corrected IN SHARED MEMORY once, when its
+// plane arrives, from a ring of coarse Corr tiles (one coarse plane per
+// step: fine block b sits on coarse index b along every axis).  The sweep
+// arithmetic is then unchanged; across a domain face a boundary point's
+// neighbour is its own ghost / wall rebuilt from its corrected value
+// (write_pads' rules), and the B points' ghosts are written from the
+// corrected box values.
 template <int EA, unsigned MASK, bool CORR = false>
-__global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUtensorMap mapH,
+__global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(const __grid_constant__ CUtensorMap mapH,
                                                    const __grid_constant__ CUtensorMap mapF,
                                                    double* __restrict__ P, Lvl L, BcSpec bc,
                                                    int chunk, const double* __restrict__ Pc = nullptr,
@@ -94,10 +111,13 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                                                    Lvl Lc = Lvl(), PeerHalo ph = PeerHalo()) {
     using namespace tsw;
     constexpr unsigned OPP = MASK ^ 0xFFu;
+    constexpr bool CC = CORR && EA < 0;   // cell: per-block constant correction
+    constexpr bool EC = CORR && EA >= 0;  // edge: prolongation, boxes corrected in smem
     extern __shared__ __align__(128) double sm[];
     double* opp = sm;                        // [4][RING][HB]
-    double* fsm = sm + 4 * RING * HB;        // [2][4][FB]
-    unsigned long long* bar = (unsigned long long*)(fsm + 2 * 4 * FB);
+    double* fsm = sm + 4 * RING * HB;        // [2][4][FB] (not EC: f from global, Fg)
+    unsigned long long* bar = (unsigned long long*)(fsm + (EC ? 0 : 2 * 4 * FB));
+    const double* __restrict__ Fg = PIc;     // (EC) this level's f
     double* csm = (double*)(bar + 2);        // (CORR) [CRING][CB] corrections, planes b0-1..b0+2
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int x0 = blockIdx.x * TX + 1, y0 = blockIdx.y * TY + 1;
@@ -116,7 +136,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
     // computed once here, so a plane step adds only the axis-0 part.
     long cofs[2] = {0, 0};
     bool cok[2] = {false, false};
-    if (CORR) {
+    if (CC) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int e = tid + i * 256;
@@ -148,12 +168,114 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
             if (e < CB) d[e] = sb(v[2 * i], v[2 * i + 1]);
         }
     };
-    if (CORR) {  // prologue: planes b0s-1, b0s, b0s+1 (all loads in flight at once)
+    if (CC) {  // prologue: planes b0s-1, b0s, b0s+1 (all loads in flight at once)
         double v[3][4];
 #pragma unroll
         for (int i = 0; i < 3; ++i) corr_fetch(b0s - 1 + i, v[i]);
 #pragma unroll
         for (int i = 0; i < 3; ++i) corr_store(b0s - 1 + i, v[i]);
+    }
+    // (EC) coarse Corr ring: entry w = (c1 - (y0-2)) * ECX + (c2 - (x0-3)) of
+    // the slot of coarse plane c0; thread tid fetches entries tid, tid+256
+    // (in-plane part of the blocked offset fixed for the launch).  Pc = Corr
+    // (k_corr_edge_in / k_corr_edge_pads: forming p_c - pinit here instead
+    // costs more in this instruction-bound kernel than the separate pass)
+    double* cring = (double*)(bar + 2);
+    int eofs[2] = {0, 0};  // (a coarse level's arrays hold < 2^31 elements)
+    bool eok[2] = {false, false};
+    if (EC) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int w = tid + i * 256;
+            const int c1 = y0 - 2 + w / ECX, c2 = x0 - 3 + w % ECX;
+            eok[i] = w < ECP && c1 >= 0 && c2 >= 0 && ((c1 + 1) >> 1) < Lc.E[1] &&
+                     ((c2 + 1) >> 1) < Lc.E[2];
+            eofs[i] = (int)((((c1 & 1) << 1) | (c2 & 1)) * Lc.cls + ((c1 + 1) >> 1) * Lc.s1 +
+                            ((c2 + 1) >> 1) + OFF);
+        }
+    }
+    auto ec_slot = [&](int c0) { return ((c0 + 2 * ERING) % ERING) * ECP; };
+    auto ec_fetch = [&](int c0, double* v) {
+        const int k0 = ((c0 + 1) >> 1) - Lc.off0;
+        const bool ok0 = c0 >= 0 && k0 >= 0 && k0 < Lc.E[0];
+        const long po = (long)((c0 & 1) << 2) * Lc.cls + (long)k0 * Lc.s0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) v[i] = (ok0 && eok[i]) ? __ldg(Pc + po + eofs[i]) : 0.0;
+    };
+    auto ec_store = [&](int c0, const double* v) {
+        double* d = cring + ec_slot(c0);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            if (tid + i * 256 < ECP) d[tid + i * 256] = v[i];
+    };
+    // correct_edge_pt's prolongation of Corr for class c at the fine block
+    // whose coarse neighbourhood starts at tile offset rc (coarse (b1-1,
+    // b2-1)) in the slots sA, sB, sC of coarse planes p-1, p, p+1 (axes
+    // permuted: edge axis P0 first)
+    auto eprol = [&](int c, int sA, int sB, int sC, int rc) -> double {
+        constexpr int P0 = EA < 0 ? 0 : EA, P1 = P0 == 0 ? 1 : 0, P2 = P0 == 2 ? 1 : 2;
+        auto cv = [&](int di, int dj, int dk) {
+            const int d0 = P0 == 0 ? di : dj;
+            const int d1 = P0 == 0 ? dj : (P0 == 1 ? di : dk);
+            const int d2 = P0 == 2 ? di : dk;
+            return cring[(d0 == 0 ? sA : (d0 == 1 ? sB : sC)) + rc + d1 * ECX + d2];
+        };
+        const int qe = (c >> (2 - P0)) & 1, qj = (c >> (2 - P1)) & 1, qk = (c >> (2 - P2)) & 1;
+        const int jd = qj ? 0 : 2, kd = qk ? 0 : 2;
+        auto line = [&](int i) {
+            const double tn = ml(ad(ml(3.0, cv(i, 1, 1)), cv(i, jd, 1)), 0.25);
+            const double tf = ml(ad(ml(3.0, cv(i, 1, kd)), cv(i, jd, kd)), 0.25);
+            return ml(ad(ml(3.0, tn), tf), 0.25);
+        };
+        return qe ? ml(ad(line(0), line(1)), 0.5) : line(1);
+    };
+    // the box entries this thread corrects (launch constants): entry w =
+    // tid + 256 i of the 34 x 10 blocks y0-1..y0+8 x x0-1..x0+32 (what the
+    // sweep reads): box offset, tile offset, and the mask of the classes to
+    // correct there -- interior points only (no pad block, no edge-axis
+    // wall), and on the halo ring only the classes a tile point reads (the
+    // row above: q1 = 0, below: q1 = 1, left: q2 = 0, right: q2 = 1; the
+    // corners: none)
+    int eb[2] = {0, 0}, er[2] = {0, 0};
+    unsigned em[2] = {0u, 0u};
+    if (EC) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int w = tid + i * 256;
+            const int j = w / (TX + 2), col = w - j * (TX + 2);
+            const int b1 = y0 - 1 + j, b2 = x0 - 1 + col;
+            unsigned m = 0xFFu;
+            if (j == 0) m &= 0x33u;
+            if (j == TY + 1) m &= 0xCCu;
+            if (col == 0) m &= 0x55u;
+            if (col == TX + 1) m &= 0xAAu;
+            if ((j == 0 || j == TY + 1) && (col == 0 || col == TX + 1)) m = 0u;
+            if (!(w < (TX + 2) * (TY + 2) && b1 >= 1 && b1 <= L.B[1] && b2 >= 1 && b2 <= L.B[2]))
+                m = 0u;
+            if (EA == 1 && b1 == L.B[1]) m &= 0xCCu;  // q1 = 0 classes: the wall
+            if (EA == 2 && b2 == L.B[2]) m &= 0xAAu;  // q2 = 0 classes: the wall
+            em[i] = m;
+            eb[i] = j * HX + col + 1;
+            er[i] = j * ECX + col + 1;
+        }
+    }
+    // add the correction to the interior points of the (class k, plane p)
+    // halo box (ring slot rs of the plane); sA..sC: slots of coarse planes
+    // p-1..p+1
+    auto ecorrect = [&](int k, int p, int rs, int sA, int sB, int sC) {
+        if (p < 1 || p > L.B[0]) return;  // pad plane: boundary points rebuild it
+        if (EA == 0 && !(k & 4) && p + L.off0 == L.G0) return;  // the wall plane
+        double* box = opp + (oslot<OPP>(k) * RING + rs) * HB;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            if ((em[i] >> k) & 1u) box[eb[i]] = ad(box[eb[i]], eprol(k, sA, sB, sC, er[i]));
+    };
+    if (EC) {  // prologue: coarse planes b0s-2 .. b0s+2
+        double v[5][2];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) ec_fetch(b0s - 2 + i, v[i]);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) ec_store(b0s - 2 + i, v[i]);
     }
 
     if (tid == 0) {
@@ -162,7 +284,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // prologue: both window planes of every opposite class + f(b0s)
         unsigned long long* br = &bar[b0s & 1];
-        mbar_expect_tx(br, 8 * HBYTES + 4 * FBYTES);
+        mbar_expect_tx(br, 8 * HBYTES + (EC ? 0 : 4 * FBYTES));
         int j = 0;
         for (int k = 0; k < 8; ++k) {
             if ((OPP >> k) & 1u) {
@@ -170,7 +292,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 for (int d = 0; d < 2; ++d)
                     tma_load4(opp + (oslot<OPP>(k) * RING + ((lo + d) % RING)) * HB, &mapH, br,
                               OFF + x0 - 2, y0 - 1, lo + d, k);
-            } else {
+            } else if (!EC) {
                 tma_load4(fsm + ((b0s & 1) * 4 + j) * FB, &mapF, br, OFF + x0, y0, b0s, k);
                 ++j;
             }
@@ -182,14 +304,14 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
     for (int b0 = b0s; b0 <= b0e; ++b0) {
         if (tid == 0 && b0 < b0e) {  // prefetch the next step's new planes + f
             unsigned long long* br = &bar[(b0 + 1) & 1];
-            mbar_expect_tx(br, 4 * HBYTES + 4 * FBYTES);
+            mbar_expect_tx(br, 4 * HBYTES + (EC ? 0 : 4 * FBYTES));
             int j = 0;
             for (int k = 0; k < 8; ++k) {
                 if ((OPP >> k) & 1u) {
                     const int nxt = ((k & 4) ? b0 : b0 - 1) + 2;
                     tma_load4(opp + (oslot<OPP>(k) * RING + (nxt % RING)) * HB, &mapH, br,
                               OFF + x0 - 2, y0 - 1, nxt, k);
-                } else {
+                } else if (!EC) {
                     tma_load4(fsm + (((b0 + 1) & 1) * 4 + j) * FB, &mapF, br, OFF + x0, y0,
                               b0 + 1, k);
                     ++j;
@@ -202,10 +324,21 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
         // (CORR) prefetch the corrections of plane b0+2 (stored at the end of
         // the step); this step's come from the shared ring
         double cpre[4] = {0.0, 0.0, 0.0, 0.0};
-        if (CORR) corr_fetch(b0 + 2, cpre);
+        if (CC) corr_fetch(b0 + 2, cpre);
+        double epre[2] = {0.0, 0.0};
+        if (EC) ec_fetch(b0 + 3, epre);  // stored at the end of the step
+        // (EC) ring slots of coarse planes b0-2 (esm), b0-1 (es0) .. b0+2 (es3)
+        int esm = 0, es0 = 0, es1 = 0, es2 = 0, es3 = 0;
+        // (EC) halo-box ring slots of planes b0-1, b0, b0+1
+        const int r0 = b0 % RING, rm = r0 == 0 ? RING - 1 : r0 - 1, rp = r0 == RING - 1 ? 0 : r0 + 1;
+        if (EC) {
+            const int t = (b0 + 2 * ERING - 2) % ERING;
+            auto sl = [&](int m) { return (t + m >= ERING ? t + m - ERING : t + m) * ECP; };
+            esm = sl(0); es0 = sl(1); es1 = sl(2); es2 = sl(3); es3 = sl(4);
+        }
         double c_own = 0.0, cW[3] = {0.0, 0.0, 0.0}, cE[3] = {0.0, 0.0, 0.0};
         double araw[8];
-        if (CORR && active) {
+        if (CC && active) {
             const int cc0 = (ty + 1) * CX + tx + 1;
             const double* cp = csm + (b0 & (CRING - 1)) * CB;
             c_own = cp[cc0];
@@ -225,7 +358,33 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 for (int c = 0; c < 8; ++c) araw[c] = 0.0;
             }
         }
+        double fv[4] = {0.0, 0.0, 0.0, 0.0};
+        if (EC && active) {  // f of the updated classes (no f boxes in this variant)
+            int j = 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if ((MASK >> c) & 1u) fv[j++] = __ldg(Fg + pl + (long)c * L.cls);
+        }
+        if (EC && active && on_boundary<3>(L, bb)) {  // own raw values: ghosts / walls
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if ((MASK >> c) & 1u) araw[c] = __ldg(P + pl + (long)c * L.cls);
+        }
         mbar_wait(&bar[b0 & 1], ((b0 - b0s) >> 1) & 1);
+        if (EC) {  // correct the planes that arrived for this step
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (!((OPP >> k) & 1u)) continue;
+                if (k & 4) {  // plane b0+1 (and b0 on the first step)
+                    ecorrect(k, b0 + 1, rp, es1, es2, es3);
+                    if (b0 == b0s) ecorrect(k, b0, r0, es0, es1, es2);
+                } else {      // plane b0 (and b0-1 on the first step)
+                    ecorrect(k, b0, r0, es0, es1, es2);
+                    if (b0 == b0s) ecorrect(k, b0 - 1, rm, esm, es0, es1);
+                }
+            }
+            __syncthreads();
+        }
         if (active) {
             const int ci = (ty + 1) * HX + tx + 2;  // tile centre in a halo box
             const bool bnd = on_boundary<3>(L, bb);
@@ -243,7 +402,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 double e0 = w0[((lo0 + 1) % RING) * HB + ci], w0v = w0[(lo0 % RING) * HB + ci];
                 double e1 = wy[ci + (q1 ? 0 : HX)], w1 = wy[ci - (q1 ? HX : 0)];
                 double e2 = wz[ci + (q2 ? 0 : 1)], w2 = wz[ci - (q2 ? 1 : 0)];
-                if (CORR) {
+                if (CC) {
                     // inside the block: own correction; across a face: the
                     // neighbour block's ...
                     if (q0) { e0 = ad(e0, c_own); w0v = ad(w0v, cW[0]); }
@@ -267,11 +426,30 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                         else if (bb[2] == Bn[2]) e2 = gh(2, 1);
                     }
                 }
+                if (EC && bnd) {  // across a domain face: own ghost / wall (write_pads)
+                    const double ac =
+                        ad(araw[c], eprol(c, es0, es1, es2,
+                                          (ty + 1) * ECX + tx + 2));
+                    auto gh = [&](int a, int sd, double raw) {
+                        const int kd = bc.kind[a][sd];
+                        if (a != EA) return kd == BC_DIRICHLET ? sb(ml(2.0, bc.val[a][sd]), ac) : ac;
+                        return kd == BC_NEUMANN ? ac : raw;
+                    };
+                    // lo face: W of a q=1 point at g=1; hi face: E of a q=0
+                    // point at g=B, or (edge axis) of the q=1 point at g=B
+                    const int g0 = gb0(L, bb);
+                    if (q0 && g0 == 1) w0v = gh(0, 0, w0v);
+                    if ((EA == 0 ? q0 : !q0) && g0 == Bn[0]) e0 = gh(0, 1, e0);
+                    if (q1 && bb[1] == 1) w1 = gh(1, 0, w1);
+                    if ((EA == 1 ? q1 : !q1) && bb[1] == Bn[1]) e1 = gh(1, 1, e1);
+                    if (q2 && bb[2] == 1) w2 = gh(2, 0, w2);
+                    if ((EA == 2 ? q2 : !q2) && bb[2] == Bn[2]) e2 = gh(2, 1, e2);
+                }
                 // ((((E+W)+N)+S)+T)+B  (KER/numpy_backend.py:62)
                 double ns = ad(e0, w0v);
                 ns = ad(ad(ns, e1), w1);
                 ns = ad(ad(ns, e2), w2);
-                nv[c] = ad(ml(L.h2, fsm[((b0 & 1) * 4 + j) * FB + tid]), ml(L.b, ns));
+                nv[c] = ad(ml(L.h2, EC ? fv[j] : fsm[((b0 & 1) * 4 + j) * FB + tid]), ml(L.b, ns));
                 ++j;
             }
 #pragma unroll
@@ -286,7 +464,7 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                 if (bnd) write_pads<3, EA>(P, L, bc, c, bb, o, nv[c]);
                 push_halo<3>(ph, L, c, bb, nv[c]);
             }
-            if (CORR && bnd) {  // ghosts of the (uncorrected in memory) B points
+            if (CC && bnd) {  // ghosts of the (uncorrected in memory) B points
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     if (!((OPP >> k) & 1u)) continue;
@@ -294,8 +472,17 @@ __global__ void __launch_bounds__(256) k_sweep_tma(const __grid_constant__ CUten
                     write_pads<3, EA>(P, L, bc, k, bb, pl + (long)k * L.cls, ad(braw, c_own));
                 }
             }
+            if (EC && bnd) {  // ghosts of the B points from their corrected (box) values
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (!((OPP >> k) & 1u) || is_wall<3, EA>(L, k, bb)) continue;
+                    const double bv = opp[(oslot<OPP>(k) * RING + (b0 % RING)) * HB + ci];
+                    write_pads<3, EA>(P, L, bc, k, bb, pl + (long)k * L.cls, bv);
+                }
+            }
         }
-        if (CORR) corr_store(b0 + 2, cpre);  // ring slot of plane b0-2: unused from now on
+        if (CC) corr_store(b0 + 2, cpre);  // ring slot of plane b0-2: unused from now on
+        if (EC) ec_store(b0 + 3, epre);    // slot of plane b0-2: unused from now on
         __syncthreads();  // the next prefetch overwrites this step's oldest slots
     }
 }

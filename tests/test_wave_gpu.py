@@ -275,3 +275,56 @@ def test_speculation_state_transitions(P, monkeypatch):
     assert np.array_equal(outs[0][0].view(np.uint64), outs[1][0].view(np.uint64))
     assert np.array_equal(outs[0][1].view(np.uint64), outs[1][1].view(np.uint64))
     np.testing.assert_allclose(outs[0][2], outs[1][2], rtol=1e-13, atol=0)
+
+
+def run_gpu_loc(P, monkeypatch, env, shape, loc, faces, p0, f0, ml, k_max, a):
+    for k, v in env.items():
+        monkeypatch.setenv(k, str(v))
+    g = P.unit_grid(shape) if len(set(shape)) == 1 else \
+        P.GridLevel(0, shape, (0.0,) * 3, tuple(s / shape[-1] for s in shape))
+    L = getattr(P.Location, LOC[loc])
+    p = P.Field(g, L, 1, p0.copy())
+    f = P.Field(g, L, 1, f0.copy())
+    _, rep = P.solve(p, f, P.OperatorCoeffs(a, 0.5), P.FasParams(1e-30, k_max, 2, ml),
+                     P.make_plan("x", 3), bc_of(P, faces))
+    torch.cuda.synchronize()
+    return p.data.cpu().numpy(), rep
+
+
+@pytest.mark.parametrize("shape,loc,spec,env,a", [
+    ((64, 64, 64), "edge_ew", "lid", {}, 1.0),
+    ((64, 64, 64), "edge_ns", "lid", {}, 1.0),
+    ((64, 64, 64), "edge_tb", "lid", {}, 1.0),
+    ((48, 112, 80), "edge_ew", "mixed_dn", {}, 1.0),                       # Neumann edge-axis wall
+    ((48, 112, 80), "edge_ns", "mixed_dn", {"FASMG_MARCH_CHUNK": 5}, 1.0),  # ragged chunks
+    ((96, 48, 80), "edge_tb", "mixed_dn", {"FASMG_MARCH_CHUNK": 3}, 1.0),
+    ((64, 64, 96), "edge_ns", "dirichlet", {"FASMG_MARCH_CHUNK": 1}, 1.0),
+    ((64, 64, 64), "edge_ew", "neumann", {}, 0.0),                         # singular
+    ((64, 64, 64), "edge_tb", "lid", {"FASMG_CORR_CHUNK": 32}, 1.0),        # one chunk
+])
+def test_edge_fused_correction_vs_oracle(P, monkeypatch, shape, loc, spec, env, a):
+    """Edge-field coarse correction fused into the first post-smoothing
+    half-sweep (k_sweep_tma<EA, M, true>: the opposite-class boxes corrected
+    in shared memory by the edge prolongation of Corr), forced onto small
+    levels over 3 V-cycles: fields bitwise equal to the oracle and to the
+    unfused k_correct_edge_fast + pad fill path, histories within 1e-10 /
+    identical."""
+    import oracle as O
+    faces = faces_of(spec) if spec in FACES else C.bc_faces(3, spec)
+    ml = 3
+    p0 = C.rand_field(63, shape, loc, 1)
+    f0 = C.rand_field(64, shape, loc, 1)
+    op = O.OField(shape, loc, 1, p0.copy())
+    of = O.OField(shape, loc, 1, f0.copy())
+    O.set_threads(8)
+    it, hist = O.fas_solve(op, of, a, 0.5, faces, O.plan_colors("x", 3), 1e-30, 3, 2, ml,
+                           dmin=0.0, dmax=shape[0] / shape[-1])
+    O.set_threads(1)
+    e = {"FASMG_TMA_MIN": 0, **env}
+    got, rep = run_gpu_loc(P, monkeypatch, e, shape, loc, faces, p0, f0, ml, 3, a)
+    np.testing.assert_allclose(rep.residual_history, hist, rtol=HIST_RTOL, atol=0)
+    assert np.array_equal(got.view(np.uint64), op.data.view(np.uint64))
+    off, rep2 = run_gpu_loc(P, monkeypatch, {**e, "FASMG_CORR_FUSE": 0}, shape, loc, faces, p0,
+                            f0, ml, 3, a)
+    assert np.array_equal(got.view(np.uint64), off.view(np.uint64))
+    assert rep.residual_history == rep2.residual_history
