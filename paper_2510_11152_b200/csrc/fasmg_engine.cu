@@ -1337,10 +1337,12 @@ static void launch_sweep_ecorr(Engine& E, int k, unsigned m, dim3 grd, dim3 blk,
     using namespace tsw;
     if (m == 0x96u)
         k_sweep_tma<A, 0x96u, true><<<grd, blk, SMEM_ECORR, E.stream>>>(
-            E.mapT[k], E.mapF[k], E.P[k], E.L[k], E.bc, chunk, E.R[k + 1], E.F[k], E.L[k + 1]);
+            E.mapT[k], E.mapF[k], E.P[k], E.L[k], E.bc, chunk, E.R[k + 1], nullptr, E.L[k + 1],
+            PeerHalo(), E.F[k]);
     else
         k_sweep_tma<A, 0x69u, true><<<grd, blk, SMEM_ECORR, E.stream>>>(
-            E.mapT[k], E.mapF[k], E.P[k], E.L[k], E.bc, chunk, E.R[k + 1], E.F[k], E.L[k + 1]);
+            E.mapT[k], E.mapF[k], E.P[k], E.L[k], E.bc, chunk, E.R[k + 1], nullptr, E.L[k + 1],
+            PeerHalo(), E.F[k]);
 }
 
 // the first post-smoothing half-sweep of level k with the coarse correction
@@ -1349,12 +1351,13 @@ static void launch_sweep_corr(Engine& E, int k, unsigned m) {
     using namespace tsw;
     const Lvl& L = E.L[k];
     const Lvl& Lc = E.L[k + 1];
-    // (edge: longer chunks amortize the per-chunk prologue of the box
-    // correction, as long as the grid keeps >= 4 waves of 3 CTAs per SM)
+    // (longer chunks amortize the per-chunk prologue of the correction
+    // ring -- for edge fields also of the box correction -- as long as the
+    // grid keeps >= 4 waves of 3 CTAs per SM)
     int chunk = E.corr_chunk > 0 ? E.corr_chunk : (E.march_chunk > 0 ? E.march_chunk : 4);
-    if (E.ea >= 0 && E.corr_chunk <= 0) {
+    if (E.corr_chunk <= 0 && E.march_chunk <= 0) {
         const long plane = (long)((L.B[2] + TX - 1) / TX) * ((L.B[1] + TY - 1) / TY);
-        for (int c = 16; c > 4; c >>= 1)
+        for (int c = E.ea >= 0 ? 16 : 8; c > 4; c >>= 1)
             if (plane * ((L.B[0] + c - 1) / c) >= 4L * 3 * E.num_sms) { chunk = c; break; }
     }
     dim3 blk(TX, TY, 1);
@@ -1363,10 +1366,12 @@ static void launch_sweep_corr(Engine& E, int k, unsigned m) {
         EA_DISPATCH(3, E.ea, (launch_sweep_ecorr<(EA < 0 ? 0 : EA)>(E, k, m, grd, blk, chunk)));
     } else if (m == 0x96u)
         k_sweep_tma<-1, 0x96u, true><<<grd, blk, SMEM_CORR, E.stream>>>(
-            E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc);
+            E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc, PeerHalo(),
+            E.F[k]);
     else
         k_sweep_tma<-1, 0x69u, true><<<grd, blk, SMEM_CORR, E.stream>>>(
-            E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc);
+            E.mapT[k], E.mapF[k], E.P[k], L, E.bc, chunk, E.P[k + 1], E.PI[k + 1], Lc, PeerHalo(),
+            E.F[k]);
 }
 
 // spec_start: the previous outer norm already ran this stage's first

@@ -61,6 +61,10 @@ __device__ __forceinline__ constexpr int oslot(int k) {
 // thread issues 8 bulk copies per step instead of every thread issuing
 // ~6 cp.async of 8 bytes, which took the issue slots of the 8-byte version.
 // Arithmetic and pad maintenance are those of k_sweep_fast.
+// edge CORR sweep: f from global (1) or TMA f boxes (0)
+#ifndef EC_FG
+#define EC_FG 0
+#endif
 namespace tsw {
 constexpr int TX = 32, TY = 8, HX = TX + 4, HY = TY + 2;
 constexpr int HB = 384;        // doubles per halo box slot (360 -> 128 B multiple)
@@ -74,8 +78,8 @@ constexpr size_t SMEM_CORR = SMEM + (size_t)CRING * CB * 8;
 // (edge CORR) coarse Corr tiles: coarse indices y0-2..y0+9 x x0-3..x0+34
 // of one coarse plane per slot, ERING planes (c0-1..c0+3 of step c0)
 constexpr int ECX = TX + 6, ECY = TY + 4, ECP = ECX * ECY, ERING = 5;
-// (f is read straight from global in that variant: no f boxes, 4 CTAs/SM)
-constexpr size_t SMEM_ECORR = SMEM - (size_t)2 * 4 * FB * 8 + (size_t)ERING * ECP * 8;
+// (f read straight from global in that variant: no f boxes)
+constexpr size_t SMEM_ECORR = SMEM - (EC_FG ? (size_t)2 * 4 * FB * 8 : 0) + (size_t)ERING * ECP * 8;
 }  // namespace tsw
 
 // CORR: this is the FIRST post-smoothing half-sweep of the level and also
@@ -102,22 +106,24 @@ constexpr size_t SMEM_ECORR = SMEM - (size_t)2 * 4 * FB * 8 + (size_t)ERING * EC
 // neighbour is its own ghost / wall rebuilt from its corrected value
 // (write_pads' rules), and the B points' ghosts are written from the
 // corrected box values.
+#define EC_BOUND ((CORR && EA >= 0) ? 3 : 0)
 template <int EA, unsigned MASK, bool CORR = false>
-__global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(const __grid_constant__ CUtensorMap mapH,
+__global__ void __launch_bounds__(256, EC_BOUND) k_sweep_tma(const __grid_constant__ CUtensorMap mapH,
                                                    const __grid_constant__ CUtensorMap mapF,
                                                    double* __restrict__ P, Lvl L, BcSpec bc,
                                                    int chunk, const double* __restrict__ Pc = nullptr,
                                                    const double* __restrict__ PIc = nullptr,
-                                                   Lvl Lc = Lvl(), PeerHalo ph = PeerHalo()) {
+                                                   Lvl Lc = Lvl(), PeerHalo ph = PeerHalo(),
+                                                   const double* __restrict__ Fg = nullptr) {
     using namespace tsw;
     constexpr unsigned OPP = MASK ^ 0xFFu;
     constexpr bool CC = CORR && EA < 0;   // cell: per-block constant correction
     constexpr bool EC = CORR && EA >= 0;  // edge: prolongation, boxes corrected in smem
+    constexpr bool FG = EC && EC_FG;      // f read from global (Fg), not TMA boxes
     extern __shared__ __align__(128) double sm[];
     double* opp = sm;                        // [4][RING][HB]
-    double* fsm = sm + 4 * RING * HB;        // [2][4][FB] (not EC: f from global, Fg)
-    unsigned long long* bar = (unsigned long long*)(fsm + (EC ? 0 : 2 * 4 * FB));
-    const double* __restrict__ Fg = PIc;     // (EC) this level's f
+    double* fsm = sm + 4 * RING * HB;        // [2][4][FB] (not FG)
+    unsigned long long* bar = (unsigned long long*)(fsm + (FG ? 0 : 2 * 4 * FB));
     double* csm = (double*)(bar + 2);        // (CORR) [CRING][CB] corrections, planes b0-1..b0+2
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int x0 = blockIdx.x * TX + 1, y0 = blockIdx.y * TY + 1;
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(co
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // prologue: both window planes of every opposite class + f(b0s)
         unsigned long long* br = &bar[b0s & 1];
-        mbar_expect_tx(br, 8 * HBYTES + (EC ? 0 : 4 * FBYTES));
+        mbar_expect_tx(br, 8 * HBYTES + (FG ? 0 : 4 * FBYTES));
         int j = 0;
         for (int k = 0; k < 8; ++k) {
             if ((OPP >> k) & 1u) {
@@ -292,7 +298,7 @@ __global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(co
                 for (int d = 0; d < 2; ++d)
                     tma_load4(opp + (oslot<OPP>(k) * RING + ((lo + d) % RING)) * HB, &mapH, br,
                               OFF + x0 - 2, y0 - 1, lo + d, k);
-            } else if (!EC) {
+            } else if (!FG) {
                 tma_load4(fsm + ((b0s & 1) * 4 + j) * FB, &mapF, br, OFF + x0, y0, b0s, k);
                 ++j;
             }
@@ -304,14 +310,14 @@ __global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(co
     for (int b0 = b0s; b0 <= b0e; ++b0) {
         if (tid == 0 && b0 < b0e) {  // prefetch the next step's new planes + f
             unsigned long long* br = &bar[(b0 + 1) & 1];
-            mbar_expect_tx(br, 4 * HBYTES + (EC ? 0 : 4 * FBYTES));
+            mbar_expect_tx(br, 4 * HBYTES + (FG ? 0 : 4 * FBYTES));
             int j = 0;
             for (int k = 0; k < 8; ++k) {
                 if ((OPP >> k) & 1u) {
                     const int nxt = ((k & 4) ? b0 : b0 - 1) + 2;
                     tma_load4(opp + (oslot<OPP>(k) * RING + (nxt % RING)) * HB, &mapH, br,
                               OFF + x0 - 2, y0 - 1, nxt, k);
-                } else if (!EC) {
+                } else if (!FG) {
                     tma_load4(fsm + (((b0 + 1) & 1) * 4 + j) * FB, &mapF, br, OFF + x0, y0,
                               b0 + 1, k);
                     ++j;
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(co
             }
         }
         double fv[4] = {0.0, 0.0, 0.0, 0.0};
-        if (EC && active) {  // f of the updated classes (no f boxes in this variant)
+        if (FG && active) {  // f of the updated classes (no f boxes in this variant)
             int j = 0;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
@@ -449,7 +455,7 @@ __global__ void __launch_bounds__(256, (CORR && EA >= 0) ? 3 : 0) k_sweep_tma(co
                 double ns = ad(e0, w0v);
                 ns = ad(ad(ns, e1), w1);
                 ns = ad(ad(ns, e2), w2);
-                nv[c] = ad(ml(L.h2, EC ? fv[j] : fsm[((b0 & 1) * 4 + j) * FB + tid]), ml(L.b, ns));
+                nv[c] = ad(ml(L.h2, FG ? fv[j] : fsm[((b0 & 1) * 4 + j) * FB + tid]), ml(L.b, ns));
                 ++j;
             }
 #pragma unroll
