@@ -28,12 +28,14 @@ ncu --set full --clock-control none --import-source on -k regex:k_resid_tma -s 2
     -o gpurun_out/${TAG}_spec python scripts/profile_vcycle.py 512 3 2 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_tau_edge -s 0 -c 1 \
     -o gpurun_out/${TAG}_etau python scripts/profile_vcycle.py 512 3 1 edge_ns > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_sweep_tma -s 24 -c 1 \
+    -o gpurun_out/${TAG}_ecorr python scripts/profile_vcycle.py 512 3 1 edge_ns > /dev/null 2>&1
 # summaries on the box (the .ncu-rep captures exceed gpurun's copy-back cap)
 mkdir -p gpurun_out/${TAG}_prof
 PROF_OUT=gpurun_out/${TAG}_prof python scripts/summarize_profiles.py ${TAG}edge > /dev/null 2>&1
 mv gpurun_out/${TAG}_prof/ncu_sweep_traffic.json gpurun_out/${TAG}_prof/ncu_sweep_traffic_edge.json 2>/dev/null
 PROF_OUT=gpurun_out/${TAG}_prof python scripts/summarize_profiles.py ${TAG} > /dev/null 2>&1
-for k in sweep tau corr etau spec; do
+for k in sweep tau corr etau spec ecorr; do
   ncu -i gpurun_out/${TAG}_${k}.ncu-rep --page details --csv > gpurun_out/${TAG}_prof/${k}_details.csv 2>/dev/null
   ncu -i gpurun_out/${TAG}_${k}.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${TAG}_prof/${k}_source.csv 2>/dev/null
 done

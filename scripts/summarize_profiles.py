@@ -74,7 +74,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
         "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
         "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
-for kind in ("sweep", "tau", "corr", "etau", "spec"):
+for kind in ("sweep", "tau", "corr", "etau", "spec", "ecorr"):
     rep = os.path.join(go, f"{tag}_{kind}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -82,7 +82,8 @@ for kind in ("sweep", "tau", "corr", "etau", "spec"):
     label = {"sweep": "finest half-sweep (k_sweep_tma)", "tau": "finest tau pass (k_resid_tma<1>)",
              "corr": "finest corrected half-sweep (k_sweep_tma<.., CORR>)",
              "etau": "finest edge-field tau pass (k_tau_edge_tma, EDGE_NS)",
-             "spec": "outer norm + next first half-sweep (k_resid_tma<2>)"}[kind]
+             "spec": "outer norm + next first half-sweep (k_resid_tma<2>)",
+             "ecorr": "finest edge corrected half-sweep (k_sweep_tma<EA, M, CORR>, EDGE_NS)"}[kind]
     out.append(f"\n# {tag}: ncu --set full, one launch: {label}")
     for k in want:
         if k in v:
