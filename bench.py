@@ -483,7 +483,9 @@ def b200_arm(args):
                                              / (ms_step * 1e-3) / 1e9}
 
     from paper_2510_11152_b200 import _native as N
-    kernels = int(N.lib().fasmg_engine_kernels_per_vcycle(eng.handle, 1))
+    # kernels per timed step: single GPU, one device-loop iteration (V-cycle
+    # + norm + k_conv, the WHILE body); slabs, V-cycle + norm
+    kernels = int(N.lib().fasmg_engine_kernels_per_vcycle(eng.handle, 2 if world == 1 else 1))
 
     # --- e2e through the public API with host buffers (single GPU: Field +
     #     solve(kMax=1); slabs: per-rank slab copies + DistSlabSolver)
@@ -607,8 +609,8 @@ def b200_arm(args):
             "roofline": roofline, "cpu_baseline": cpu,
             "cpu_baseline_reference_1core": numba, "e2e": e2e,
             "clocks": clocks.summary(),
-            "gpu_launches": (kernels + (1 if world == 1 else 0)) * K,
-            "kernels_per_step": kernels + (1 if world == 1 else 0),
+            "gpu_launches": kernels * K,
+            "kernels_per_step": kernels,
             "solve_loop": ("one graph launch for the K iterations (conditional WHILE node, "
                            "device-side residual test k_conv)" if world == 1 else
                            "per-iteration launch + host read"),

@@ -207,6 +207,8 @@ int fasmg_engine_store(void* engine, double* pcore, const long* ps);
  * CUDA graph */
 int fasmg_engine_run(void* engine, int count, int with_norm, double* sumsq, int use_graph);
 int fasmg_engine_residual_sumsq(void* engine, double* sumsq);
+/* kernels per captured V-cycle (with_norm 0/1), or per iteration of the
+ * device solve loop (with_norm 2: V-cycle + norm + convergence test) */
 long fasmg_engine_kernels_per_vcycle(void* engine, int with_norm);
 /* mean duration (ms, CUDA events on the engine stream) of one smoothing
  * half-sweep launch on `level`, over `reps` launches */

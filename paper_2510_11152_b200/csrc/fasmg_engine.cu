@@ -37,6 +37,7 @@
 // graph and replayed per outer iteration.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <limits.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -896,6 +897,7 @@ struct Engine {
     cudaGraphExec_t execs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     long kernels_per_vcycle = 0;
     long kernels_per_vcycle_norm = 0;
+    long kernels_per_solve_iter = 0;    // a device-loop iteration in steady state (k_conv included)
     // 0: thread per block, 1: per (block, class), 2: 2.5D register march,
     // 3: 2.5D shared-memory march (cp.async) for large 3D levels, 4: the
     // same march fed by TMA boxes (default), else 0
@@ -989,8 +991,8 @@ static bool resid_tma_level(const Engine& E, int k) {
 // face, first two half-sweeps complementary X/RBGS color groups
 static bool corr_fused(const Engine& E, int k) {
     if (!E.corr_fuse || E.dim != 3 || E.ea >= 0 || !E.tma_ok[k] || E.sharded(k) ||
-        k + 1 >= E.nl || !E.PI[k + 1] || E.masks.size() < 2)
-        return false;
+        k + 1 >= E.nl || !E.PI[k + 1] || E.masks.size() < 2 || 8 * E.L[k + 1].cls >= INT_MAX)
+        return false;  // (the kernel addresses the coarse level with 32-bit offsets)
     for (int a = 0; a < 3; ++a)
         if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
     const unsigned m0 = E.masks[0], m1 = E.masks[1];
@@ -1002,7 +1004,7 @@ static bool corr_fused(const Engine& E, int k) {
 // and boundary conditions as corr_fused, the edge_fast transfers
 static bool ecorr_fused(const Engine& E, int k) {
     if (!E.corr_fuse || E.dim != 3 || E.ea < 0 || !E.edge_fast || !E.tma_ok[k] ||
-        E.sharded(k) || k + 1 >= E.nl || E.masks.size() < 2)
+        E.sharded(k) || k + 1 >= E.nl || E.masks.size() < 2 || 8 * E.L[k + 1].cls >= INT_MAX)
         return false;
     for (int a = 0; a < 3; ++a)
         if (E.bc.kind[a][0] == BC_PERIODIC || E.bc.kind[a][1] == BC_PERIODIC) return false;
@@ -1680,6 +1682,7 @@ static void capture_iteration(Engine& E, bool pending, cudaGraphConditionalHandl
     launch_norm<D>(E, cnt);
     E.cap_pending = E.cap_spec = false;
     k_conv<<<1, 1, 0, E.stream>>>(E.dsum, E.dctl, E.dhist, E.dit, h);
+    if (pending) E.kernels_per_solve_iter = cnt + 1;  // the WHILE body
 }
 
 // [first iteration (from the current speculation state)] -> WHILE(cond) {
@@ -2526,6 +2529,8 @@ int fasmg_engine_time_sweeps(void* h, int k, int reps, double* ms) {
 // counted while building the graph; 0 before the first captured run
 long fasmg_engine_kernels_per_vcycle(void* h, int with_norm) {
     Engine* E = (Engine*)h;
+    // with_norm 2: one iteration of the device solve loop (fasmg_engine_solve)
+    if (with_norm == 2) return E->kernels_per_solve_iter;
     return with_norm ? E->kernels_per_vcycle_norm : E->kernels_per_vcycle;
 }
 

@@ -187,26 +187,25 @@ __global__ void __launch_bounds__(256, EC_BOUND) k_sweep_tma(const __grid_consta
     // (k_corr_edge_in / k_corr_edge_pads: forming p_c - pinit here instead
     // costs more in this instruction-bound kernel than the separate pass)
     double* cring = (double*)(bar + 2);
-    int eofs[2] = {0, 0};  // (a coarse level's arrays hold < 2^31 elements)
-    bool eok[2] = {false, false};
+    int eofs[2] = {-1, -1};  // (32-bit, -1: outside the level; as cofs)
     if (EC) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int w = tid + i * 256;
             const int c1 = y0 - 2 + w / ECX, c2 = x0 - 3 + w % ECX;
-            eok[i] = w < ECP && c1 >= 0 && c2 >= 0 && ((c1 + 1) >> 1) < Lc.E[1] &&
-                     ((c2 + 1) >> 1) < Lc.E[2];
-            eofs[i] = (int)((((c1 & 1) << 1) | (c2 & 1)) * Lc.cls + ((c1 + 1) >> 1) * Lc.s1 +
-                            ((c2 + 1) >> 1) + OFF);
+            if (w < ECP && c1 >= 0 && c2 >= 0 && ((c1 + 1) >> 1) < Lc.E[1] &&
+                ((c2 + 1) >> 1) < Lc.E[2])
+                eofs[i] = (((c1 & 1) << 1) | (c2 & 1)) * (int)Lc.cls + ((c1 + 1) >> 1) * (int)Lc.s1 +
+                          ((c2 + 1) >> 1) + OFF;
         }
     }
     auto ec_slot = [&](int c0) { return ((c0 + 2 * ERING) % ERING) * ECP; };
     auto ec_fetch = [&](int c0, double* v) {
         const int k0 = ((c0 + 1) >> 1) - Lc.off0;
         const bool ok0 = c0 >= 0 && k0 >= 0 && k0 < Lc.E[0];
-        const long po = (long)((c0 & 1) << 2) * Lc.cls + (long)k0 * Lc.s0;
+        const int po = ((c0 & 1) << 2) * (int)Lc.cls + k0 * (int)Lc.s0;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) v[i] = (ok0 && eok[i]) ? __ldg(Pc + po + eofs[i]) : 0.0;
+        for (int i = 0; i < 2; ++i) v[i] = (ok0 && eofs[i] >= 0) ? __ldg(Pc + (po + eofs[i])) : 0.0;
     };
     auto ec_store = [&](int c0, const double* v) {
         double* d = cring + ec_slot(c0);
