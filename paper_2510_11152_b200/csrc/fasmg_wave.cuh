@@ -30,6 +30,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
         "r"(parity)
         : "memory");
+    // the lanes of a warp can leave the spin at different polls: reconverge
+    // before the caller's next block barrier.  Every caller waits with all
+    // 32 lanes.
+    __syncwarp();
 }
 __device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map,
                                           unsigned long long* bar, int c0, int c1, int c2,

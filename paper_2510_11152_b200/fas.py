@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -29,6 +30,11 @@ from .errors import NativeError
 from .grid import Field, GridHierarchy, Location, make_hierarchy, subtract_interior_mean
 from .smoothers import SweepPlan
 from .stencil import OperatorCoeffs
+
+# FASMG_DEVICE_LOOP=0: the outer loop on the host, one graph launch per
+# iteration (the device loop's conditional graph node is not supported by
+# compute-sanitizer's racecheck / synccheck)
+_DEVICE_LOOP = os.environ.get("FASMG_DEVICE_LOOP", "1") != "0"
 
 
 @dataclass(frozen=True)
@@ -249,7 +255,7 @@ class FasSolver:
         g = self.hierarchy.fine
         scale = g.h ** (g.dim / 2.0)
         history: list = []
-        if self.use_graph and 1 <= params.k_max <= 4096:
+        if self.use_graph and _DEVICE_LOOP and 1 <= params.k_max <= 4096:
             # the loop below, with the test on the device: one graph launch
             history = e.solve_loop(params.k_max, params.tol, scale)
         else:

@@ -1,0 +1,10 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r02bh; mkdir -p $O
+for tool in synccheck racecheck; do
+  for case in tma edge; do
+    timeout 600 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_cases.py $case > $O/san_${tool}_${case}_dl.log 2>&1
+    echo "rc=$?" >> $O/san_${tool}_${case}_dl.log
+  done
+done
+for l in cell ew; do timeout 300 python scripts/vcycle_prof.py 512 $l 5 > $O/prof_$l.txt 2>&1; done
