@@ -135,3 +135,30 @@ def test_solver_solve_uses_device_loop_vs_oracle(P):
     np.testing.assert_allclose(ra.residual_history, hist, rtol=1e-10, atol=0)
     assert np.array_equal(a.view(np.uint64), op.data.view(np.uint64))
     assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("k_max,tol", [(3, float("nan")), (5000, 1e-6), (1, 1e-30)])
+def test_solver_solve_device_vs_host_loop_edge_cases(P, monkeypatch, k_max, tol):
+    """FasSolver.solve with the device loop against FASMG_DEVICE_LOOP=0 (the
+    host loop): a NaN tolerance (never met: k_max cycles, as the host's
+    `res <= tol` test), a k_max above the device loop's cap (the host loop
+    runs; iterations stop on tol), a single cycle."""
+    from paper_2510_11152_b200 import fas
+    shape = (32, 32, 32)
+    g, S = make(P, shape)
+    p0 = C.rand_field(77, shape, "cell", 1)
+    f0 = C.rand_field(78, shape, "cell", 1)
+    outs = []
+    for dev in (True, False):
+        monkeypatch.setattr(fas, "_DEVICE_LOOP", dev)
+        p = P.Field(g, P.Location.CELL, 1, p0.copy())
+        f = P.Field(g, P.Location.CELL, 1, f0.copy())
+        rep = S.solve(p, f, P.FasParams(tol, k_max, 2, 3))
+        torch.cuda.synchronize()
+        outs.append((p.data.cpu().numpy(), rep))
+    (a, ra), (b, rb) = outs
+    assert ra.residual_history == rb.residual_history
+    assert ra.iterations == rb.iterations
+    if tol != tol:
+        assert ra.iterations == k_max
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
