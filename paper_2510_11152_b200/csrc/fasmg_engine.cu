@@ -372,14 +372,23 @@ __device__ __forceinline__ void pad_all_pt(double* __restrict__ P, const Lvl& L,
         ax[q].edge = (q == L.ea);
     }
     BlkReader<D> rd{P, L};
+    // all classes' ghost values before any store: the chains end in reads
+    // of interior points (or the never-written periodic low wall), never in
+    // a slot written here, so their loads can all be in flight at once
+    double v[1 << D];
+    unsigned todo = 0u;
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
         int x[3] = {0, 0, 0};
         bool in;
+        v[c] = 0.0;
         if (!grid_idx<D>(L, c, b, x, &in) || in) continue;
-        const double v = ghost_value<D>(ax, bc, x[0], x[1], x[2], rd);
-        P[at<D>(L, c, b[0], b[1], b[2])] = v;
+        todo |= 1u << c;
+        v[c] = ghost_value<D>(ax, bc, x[0], x[1], x[2], rd);
     }
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c)
+        if ((todo >> c) & 1u) P[at<D>(L, c, b[0], b[1], b[2])] = v[c];
 }
 
 // grid: x over the face's last other axis (3D; 2D: the other axis), y over
@@ -511,16 +520,21 @@ __device__ __forceinline__ void corr_edge_pt(const double* __restrict__ Pc,
     bool inner_blk = skip_inner;
 #pragma unroll
     for (int a = 0; a < D; ++a) inner_blk = inner_blk && b[a] >= 1 && b[a] <= Lc.B[a];
+    // values of every class first, then the stores (the loads in flight
+    // together)
+    double v[1 << D];
+    unsigned todo = 0u;
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
         int x[3] = {0, 0, 0};
         bool in;
+        v[c] = 0.0;
         if (!grid_idx<D>(Lc, c, b, x, &in)) continue;
         if (inner_blk && in) continue;
+        todo |= 1u << c;
         const long o = o0 + (long)c * Lc.cls;
-        double v;
         if (in) {
-            v = sb(Pc[o], PI[o]);
+            v[c] = sb(Pc[o], PI[o]);
         } else {
             AxisGeo ax[3];
 #pragma unroll
@@ -528,10 +542,12 @@ __device__ __forceinline__ void corr_edge_pt(const double* __restrict__ Pc,
                 ax[q].m = q < D ? Lc.n[q] : 1;
                 ax[q].edge = (q == Lc.ea);
             }
-            v = ghost_value<D>(ax, bch, x[0], x[1], x[2], rd);
+            v[c] = ghost_value<D>(ax, bch, x[0], x[1], x[2], rd);
         }
-        Corr[o] = v;
     }
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c)
+        if ((todo >> c) & 1u) Corr[o0 + (long)c * Lc.cls] = v[c];
 }
 
 // The interior part of Corr (the common case of corr_edge_pt), on the block

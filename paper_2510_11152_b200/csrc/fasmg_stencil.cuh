@@ -171,6 +171,13 @@ __device__ __forceinline__ void pad_fill_pt(double* __restrict__ P, const Lvl& L
     bb[oth[0]] = 1 + i1;
     if (D == 3) bb[oth[1]] = 1 + i2;
     const long o0 = at<D>(L, 0, bb[0], bb[1], bb[2]);
+    // every class's value first: the loads go out together instead of one
+    // L2 round trip per class behind the previous class's pad stores (no
+    // slot read here is written below: a wall slot written for class c is
+    // skipped as c's own point)
+    double pv[1 << D];
+#pragma unroll
+    for (int c = 0; c < (1 << D); ++c) pv[c] = P[o0 + (long)c * L.cls];
 #pragma unroll
     for (int c = 0; c < (1 << D); ++c) {
         const long o = o0 + (long)c * L.cls;
@@ -186,7 +193,7 @@ __device__ __forceinline__ void pad_fill_pt(double* __restrict__ P, const Lvl& L
             }
         }
         if (is_wall<D, EA>(L, c, bb)) continue;
-        write_pads<D, EA>(P, L, bc, c, bb, o, P[o]);
+        write_pads<D, EA>(P, L, bc, c, bb, o, pv[c]);
     }
 }
 
