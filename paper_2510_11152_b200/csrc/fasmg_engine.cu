@@ -960,6 +960,7 @@ struct Engine {
     double* hbuf = nullptr;             // pinned: ctl (3) + history (SOLVE_CAP) + count
     int corr_chunk = 0;                 // FASMG_CORR_CHUNK: planes per CTA of that sweep (0: march chunk)
     int num_sms = 148;
+    int tau_chunk = 0, norm_chunk = 0;  // FASMG_TAU_CHUNK / FASMG_NORM_CHUNK (0: 4 planes)
     int chunk_l1 = 2;                   // FASMG_CHUNK_L1: TMA sweep chunk on levels >= 1 (2: twice
                                         // the CTAs of 4 -- a shorter tail, 38.5 -> 38.0 us at 256^3)
     int edge_tau = 1;                   // FASMG_EDGE_TAU: edge-field tau pass in one march (k_tau_edge_tma)
@@ -1454,7 +1455,7 @@ static void launch_vcycle(Engine& E, long& cnt) {
         if (E.ea < 0) {
             {
                 if (D == 3 && resid_tma_level(E, k)) {
-                    const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+                    const int ch = E.march_chunk > 0 ? E.march_chunk : (E.tau_chunk > 0 ? E.tau_chunk : 4);
                     if (E.resid_pf)
                         k_resid_tma<1, -1, true><<<resid_grid(L, ch), dim3(rsw::TX, rsw::TY, 1),
                                                    rsw::SMEM, E.stream>>>(
@@ -1572,7 +1573,7 @@ static void launch_norm(Engine& E, long& cnt) {
     const Tile t = tile_of(L);
     int npart_norm = E.npart;
     if (D == 3 && E.cap_spec) {  // norm + the next V-cycle's first half-sweep (into P2)
-        const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+        const int ch = E.march_chunk > 0 ? E.march_chunk : (E.norm_chunk > 0 ? E.norm_chunk : 4);
         const dim3 g = resid_grid(L, ch), b(rsw::TX, rsw::TY, 1);
         if (E.masks[0] == 0x96u)
             k_resid_tma<2, -1, true, 0x96u><<<g, b, E.norm_smem, E.stream>>>(
@@ -1586,7 +1587,7 @@ static void launch_norm(Engine& E, long& cnt) {
         ++cnt;
     } else {
         if (D == 3 && E.resid_tma && E.tma_ok[0]) {
-            const int ch = E.march_chunk > 0 ? E.march_chunk : 4;
+            const int ch = E.march_chunk > 0 ? E.march_chunk : (E.norm_chunk > 0 ? E.norm_chunk : 4);
             const dim3 g = resid_grid(L, ch);
             if (E.resid_pf)
                 EA_DISPATCH(3, E.ea, (k_resid_tma<0, EA, true><<<g, dim3(rsw::TX, rsw::TY, 1),
@@ -1891,6 +1892,8 @@ static int tma_setup(Engine& E) {
     if (const char* v = getenv("FASMG_CORR_FUSE")) E.corr_fuse = atoi(v);
     if (const char* v = getenv("FASMG_CORR_CHUNK")) E.corr_chunk = atoi(v);
     if (const char* v = getenv("FASMG_CHUNK_L1")) E.chunk_l1 = atoi(v);
+    if (const char* v = getenv("FASMG_TAU_CHUNK")) E.tau_chunk = atoi(v);
+    if (const char* v = getenv("FASMG_NORM_CHUNK")) E.norm_chunk = atoi(v);
     {
         int dev = 0, n = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
