@@ -2447,12 +2447,12 @@ int fasmg_engine_solve(void* h, int k_max, double tol, double scale, double* his
     if (E->nranks > 1) return fasmg_set_error(FASMG_EINVAL, "device solve loop: single-rank engines only");
     if (k_max < 1 || k_max > SOLVE_CAP) return fasmg_set_error(FASMG_EINVAL, "k_max out of range");
     int st;
-    if (!E->dhist) {
-        if ((st = fasmg_check(cudaMalloc(&E->dhist, sizeof(double) * SOLVE_CAP)))) return st;
-        if ((st = fasmg_check(cudaMalloc(&E->dit, sizeof(int))))) return st;
-        if ((st = fasmg_check(cudaMalloc(&E->dctl, sizeof(double) * 3)))) return st;
-        if ((st = fasmg_check(cudaMallocHost(&E->hbuf, sizeof(double) * (SOLVE_CAP + 4))))) return st;
-    }
+    // (each buffer on its own: a failed allocation is retried by the next call)
+    if (!E->dhist && (st = fasmg_check(cudaMalloc(&E->dhist, sizeof(double) * SOLVE_CAP)))) return st;
+    if (!E->dit && (st = fasmg_check(cudaMalloc(&E->dit, sizeof(int))))) return st;
+    if (!E->dctl && (st = fasmg_check(cudaMalloc(&E->dctl, sizeof(double) * 3)))) return st;
+    if (!E->hbuf && (st = fasmg_check(cudaMallocHost(&E->hbuf, sizeof(double) * (SOLVE_CAP + 4)))))
+        return st;
     const int ps = E->spec_ok && E->spec_pending ? 1 : 0;
     if (!E->xsolve[ps] && (st = build_solve_graph(*E, ps))) return st;
     E->hbuf[0] = tol;
@@ -2463,8 +2463,10 @@ int fasmg_engine_solve(void* h, int k_max, double tol, double scale, double* his
     if ((st = fasmg_check(cudaMemsetAsync(E->dit, 0, sizeof(int), E->stream)))) return st;
     if ((st = fasmg_check(cudaGraphLaunch(E->xsolve[ps], E->stream)))) return st;
     int* hcount = (int*)(E->hbuf + SOLVE_CAP + 3);
-    cudaMemcpyAsync(hcount, E->dit, sizeof(int), cudaMemcpyDeviceToHost, E->stream);
-    cudaMemcpyAsync(E->hbuf + 3, E->dhist, sizeof(double) * k_max, cudaMemcpyDeviceToHost, E->stream);
+    if ((st = fasmg_check(cudaMemcpyAsync(hcount, E->dit, sizeof(int), cudaMemcpyDeviceToHost,
+                                          E->stream)))) return st;
+    if ((st = fasmg_check(cudaMemcpyAsync(E->hbuf + 3, E->dhist, sizeof(double) * k_max,
+                                          cudaMemcpyDeviceToHost, E->stream)))) return st;
     if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
     E->spec_pending = E->spec_ok;  // every iteration ended with the fused norm
     *iters = *hcount;
