@@ -386,7 +386,12 @@ def b200_arm(args):
         scale_res = g.h ** (dim / 2.0)
         # K outer iterations as FasSolver.solve runs them: one graph launch,
         # the residual test on the device (tol -1: never met, so exactly K)
-        run_steps = lambda k: eng.solve_loop(k, -1.0, scale_res)  # noqa: E731
+        def run_steps(k):  # (in launches of at most 4096 iterations, the loop's cap)
+            out = []
+            while k > 0:
+                out += eng.solve_loop(min(k, 4096), -1.0, scale_res)
+                k -= min(k, 4096)
+            return out
         stream_handle = eng.stream.value
         local_dof = dof
         slab_detail = None
