@@ -246,10 +246,16 @@ int fasmg_engine_prepare(void* engine, int with_norm);
 /* the whole outer solve loop (PKG/fas.py:147-154) as ONE graph launch: up to
  * k_max V-cycles + norms on the loaded state, the convergence test
  * res = scale*sqrt(sumsq) <= tol evaluated on the device (a WHILE
- * conditional node); history (host, k_max doubles) and *iters out.
- * Single-rank engines. */
+ * conditional node); history (host, k_max doubles) and *iters out. */
 int fasmg_engine_solve(void* engine, int k_max, double tol, double scale, double* history,
                        int* iters);
+/* fasmg_engine_solve in two halves for slab ranks that must all be enqueued
+ * before any is waited on (ranks on one device): capture the loop's graph on
+ * every rank first (prepare_solve), then launch each, then wait each.  All
+ * ranks see the same rank-ordered norm and stop together. */
+int fasmg_engine_prepare_solve(void* engine);
+int fasmg_engine_solve_launch(void* engine, int k_max, double tol, double scale);
+int fasmg_engine_solve_wait(void* engine, double* history, int* iters);
 /* self-test of the sweep kernels' reciprocal division: n random normal
  * numerators (|exponent| <= emax) x nd divisors; *bad = quotients whose bits
  * differ from IEEE division (expected 0) */

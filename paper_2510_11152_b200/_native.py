@@ -63,6 +63,9 @@ _SIGS = {
     "fasmg_engine_launch": "vii",
     "fasmg_engine_prepare": "vi",
     "fasmg_engine_solve": "viddDI",
+    "fasmg_engine_prepare_solve": "v",
+    "fasmg_engine_solve_launch": "vidd",
+    "fasmg_engine_solve_wait": "vDI",
     "fasmg_selftest_div": "llDiiL",
     "fasmg_engine_level_geom": "viL",
     "fasmg_engine_level_copy": "viip",

@@ -2440,21 +2440,37 @@ int fasmg_engine_prepare(void* h, int with_norm) {
 // A whole outer solve loop (PKG/fas.py:147-154) as one graph launch: up to
 // k_max V-cycles + norms on the loaded state, stopping on the device at the
 // first res = scale*sqrt(sumsq) <= tol.  history: host array of k_max doubles;
-// *iters = V-cycles run.  Single-rank engines (slab ranks loop on the host).
-int fasmg_engine_solve(void* h, int k_max, double tol, double scale, double* history,
-                       int* iters) {
+// *iters = V-cycles run.  Slab ranks: every rank's norm is the same
+// rank-ordered sum, so the ranks stop together.
+//
+// the device loop's buffers (each on its own: a failed allocation is
+// retried by the next call) and its graph for the current speculation state
+static int solve_prepare(Engine& E) {
+    int st;
+    if (!E.dhist && (st = fasmg_check(cudaMalloc(&E.dhist, sizeof(double) * SOLVE_CAP)))) return st;
+    if (!E.dit && (st = fasmg_check(cudaMalloc(&E.dit, sizeof(int))))) return st;
+    if (!E.dctl && (st = fasmg_check(cudaMalloc(&E.dctl, sizeof(double) * 3)))) return st;
+    if (!E.hbuf && (st = fasmg_check(cudaMallocHost(&E.hbuf, sizeof(double) * (SOLVE_CAP + 4)))))
+        return st;
+    const int ps = E.spec_ok && E.spec_pending ? 1 : 0;
+    if (!E.xsolve[ps] && (st = build_solve_graph(E, ps))) return st;
+    return 0;
+}
+
+// Capture the device loop's graph before any rank launches (slab ranks on
+// one device: a capture that lazily loads a module waits for running
+// kernels, i.e. for peers spinning on this rank -- see fasmg_engine_prepare).
+int fasmg_engine_prepare_solve(void* h) { return solve_prepare(*(Engine*)h); }
+
+// Enqueue the device loop (no host synchronization): slab ranks enqueue on
+// every rank first, then wait.  Every rank's norm is the same rank-ordered
+// sum (launch_norm), so all ranks take the same decisions in lockstep.
+int fasmg_engine_solve_launch(void* h, int k_max, double tol, double scale) {
     Engine* E = (Engine*)h;
-    if (E->nranks > 1) return fasmg_set_error(FASMG_EINVAL, "device solve loop: single-rank engines only");
     if (k_max < 1 || k_max > SOLVE_CAP) return fasmg_set_error(FASMG_EINVAL, "k_max out of range");
     int st;
-    // (each buffer on its own: a failed allocation is retried by the next call)
-    if (!E->dhist && (st = fasmg_check(cudaMalloc(&E->dhist, sizeof(double) * SOLVE_CAP)))) return st;
-    if (!E->dit && (st = fasmg_check(cudaMalloc(&E->dit, sizeof(int))))) return st;
-    if (!E->dctl && (st = fasmg_check(cudaMalloc(&E->dctl, sizeof(double) * 3)))) return st;
-    if (!E->hbuf && (st = fasmg_check(cudaMallocHost(&E->hbuf, sizeof(double) * (SOLVE_CAP + 4)))))
-        return st;
+    if ((st = solve_prepare(*E))) return st;
     const int ps = E->spec_ok && E->spec_pending ? 1 : 0;
-    if (!E->xsolve[ps] && (st = build_solve_graph(*E, ps))) return st;
     E->hbuf[0] = tol;
     E->hbuf[1] = scale;
     E->hbuf[2] = (double)k_max;
@@ -2467,11 +2483,26 @@ int fasmg_engine_solve(void* h, int k_max, double tol, double scale, double* his
                                           E->stream)))) return st;
     if ((st = fasmg_check(cudaMemcpyAsync(E->hbuf + 3, E->dhist, sizeof(double) * k_max,
                                           cudaMemcpyDeviceToHost, E->stream)))) return st;
-    if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
-    E->spec_pending = E->spec_ok;  // every iteration ended with the fused norm
-    *iters = *hcount;
-    for (int i = 0; i < *hcount; ++i) history[i] = E->hbuf[3 + i];
+    E->spec_pending = E->spec_ok;  // every iteration ends with the fused norm
     return 0;
+}
+
+// Wait for the loop fasmg_engine_solve_launch enqueued; its history (host,
+// up to k_max doubles) and iteration count.
+int fasmg_engine_solve_wait(void* h, double* history, int* iters) {
+    Engine* E = (Engine*)h;
+    int st;
+    if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
+    const int n = *(const int*)(E->hbuf + SOLVE_CAP + 3);
+    *iters = n;
+    for (int i = 0; i < n; ++i) history[i] = E->hbuf[3 + i];
+    return 0;
+}
+
+int fasmg_engine_solve(void* h, int k_max, double tol, double scale, double* history,
+                       int* iters) {
+    int st = fasmg_engine_solve_launch(h, k_max, tol, scale);
+    return st ? st : fasmg_engine_solve_wait(h, history, iters);
 }
 
 int fasmg_engine_result(void* h, double* sumsq) {

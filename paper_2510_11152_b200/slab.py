@@ -138,6 +138,21 @@ class _SlabEngine:
         N.call("fasmg_engine_result", self.handle, ctypes.byref(out))
         return out.value
 
+    # the device solve loop (fasmg_engine_solve in halves: every rank is
+    # prepared, then launched, then waited on)
+    def prepare_solve(self):
+        N.call("fasmg_engine_prepare_solve", self.handle)
+
+    def solve_launch(self, k_max: int, tol: float, scale: float):
+        self._kmax = int(k_max)
+        N.call("fasmg_engine_solve_launch", self.handle, int(k_max), float(tol), float(scale))
+
+    def solve_wait(self) -> list:
+        hist = (ctypes.c_double * self._kmax)()
+        n = ctypes.c_int(0)
+        N.call("fasmg_engine_solve_wait", self.handle, hist, ctypes.byref(n))
+        return list(hist[: n.value])
+
     def synchronize(self):
         N.call("fasmg_stream_synchronize", self.stream)
 
@@ -256,6 +271,36 @@ class VirtualSlabSolver:
             N.call("fasmg_sub_mean", N.ptr(v), N.strides(v), v.dim(), N.ints(v.shape),
                    N.ptr(tot), float(math.prod(gext)), N.torch_stream())
 
+    def _outer_loop(self, es, params: FasParams, scale: float) -> list:
+        """The outer loop of FasSolver.solve over the virtual ranks: the
+        device loop on every rank (all graphs captured, then all launched,
+        then waited on: a rank's loop stalls until its peers run), or the
+        host loop (FASMG_DEVICE_LOOP=0, kMax above the device loop's cap, or
+        more than 4 ranks: 8 ranks' spinning loops on ONE device outrun its
+        hardware queues and stall -- a one-device artefact, real ranks each
+        have their own GPU)."""
+        from . import fas as _fas
+        if _fas._DEVICE_LOOP and 1 <= params.k_max <= 4096 and len(es) <= 4:
+            for e in es:
+                e.prepare_solve()
+            for e in es:
+                e.solve_launch(params.k_max, params.tol, scale)
+            hists = [e.solve_wait() for e in es]
+            if any(h != hists[0] for h in hists):
+                raise NativeError(f"ranks disagree on the residual history: {hists}")
+            return hists[0]
+        history = []
+        for _ in range(params.k_max):
+            self.launch_all(es, 1, True)
+            sums = [e.result() for e in es]
+            if any(x != sums[0] for x in sums):
+                raise NativeError(f"ranks disagree on the residual: {sums}")
+            res = scale * math.sqrt(sums[0])
+            history.append(res)
+            if res <= params.tol:
+                break
+        return history
+
     def solve_views(self, pvs, fvs, params: FasParams, halo_p: int = 1,
                     halo_f: int = 1) -> SolveReport:
         """``solve`` on per-rank slab views (rank cells + 1 ghost plane each
@@ -274,16 +319,7 @@ class VirtualSlabSolver:
             e.sync_halos()
         g = self.hierarchy.fine
         scale = g.h ** (g.dim / 2.0)
-        history = []
-        for _ in range(params.k_max):
-            self.launch_all(es, 1, True)
-            sums = [e.result() for e in es]
-            if any(x != sums[0] for x in sums):
-                raise NativeError(f"ranks disagree on the residual: {sums}")
-            res = scale * math.sqrt(sums[0])
-            history.append(res)
-            if res <= params.tol:
-                break
+        history = self._outer_loop(es, params, scale)
         for e, pv in zip(es, pvs):
             e.store(pv, halo_p)
         if singular:
@@ -298,16 +334,7 @@ class VirtualSlabSolver:
         self._load(es, p, f)
         g = self.hierarchy.fine
         scale = g.h ** (g.dim / 2.0)
-        history = []
-        for _ in range(params.k_max):
-            self.launch_all(es, 1, True)
-            sums = [e.result() for e in es]
-            if any(x != sums[0] for x in sums):
-                raise NativeError(f"ranks disagree on the residual: {sums}")
-            res = scale * math.sqrt(sums[0])
-            history.append(res)
-            if res <= params.tol:
-                break
+        history = self._outer_loop(es, params, scale)
         self._store(es, p)
         fill_ghosts(p, self.bc)
         if singular:
@@ -433,13 +460,27 @@ class DistSlabSolver:
         g = self.hierarchy.fine
         return g.h ** (g.dim / 2.0) * math.sqrt(sumsq)
 
+    def solve_loop(self, k_max: int, tol: float) -> list:
+        """Up to k_max V-cycles + global norms in one device-loop launch per
+        rank (every rank captured first, then a barrier: no rank's loop runs
+        while a peer still captures); all ranks stop together."""
+        g = self.hierarchy.fine
+        self.engine.prepare_solve()
+        self.dist.barrier(group=self.group)
+        self.engine.solve_launch(k_max, tol, g.h ** (g.dim / 2.0))
+        return self.engine.solve_wait()
+
     def solve_loaded(self, params: FasParams) -> SolveReport:
-        history = []
-        for _ in range(params.k_max):
-            res = self.run(1)
-            history.append(res)
-            if res <= params.tol:
-                break
+        from . import fas as _fas
+        if _fas._DEVICE_LOOP and 1 <= params.k_max <= 4096:
+            history = self.solve_loop(params.k_max, params.tol)
+        else:
+            history = []
+            for _ in range(params.k_max):
+                res = self.run(1)
+                history.append(res)
+                if res <= params.tol:
+                    break
         return SolveReport(len(history), history, bool(history and history[-1] <= params.tol))
 
     def store(self, pv: torch.Tensor, halo_p: int = 1):
