@@ -2491,6 +2491,7 @@ int fasmg_engine_solve_launch(void* h, int k_max, double tol, double scale) {
 // up to k_max doubles) and iteration count.
 int fasmg_engine_solve_wait(void* h, double* history, int* iters) {
     Engine* E = (Engine*)h;
+    if (!E->hbuf) return fasmg_set_error(FASMG_EINVAL, "no device solve loop was launched");
     int st;
     if ((st = fasmg_check(cudaStreamSynchronize(E->stream)))) return st;
     const int n = *(const int*)(E->hbuf + SOLVE_CAP + 3);

@@ -143,11 +143,15 @@ class _SlabEngine:
     def prepare_solve(self):
         N.call("fasmg_engine_prepare_solve", self.handle)
 
+    _kmax = 0  # k_max of the last solve_launch (the history length bound)
+
     def solve_launch(self, k_max: int, tol: float, scale: float):
         self._kmax = int(k_max)
         N.call("fasmg_engine_solve_launch", self.handle, int(k_max), float(tol), float(scale))
 
     def solve_wait(self) -> list:
+        if self._kmax < 1:
+            raise NativeError("solve_wait without a solve_launch")
         hist = (ctypes.c_double * self._kmax)()
         n = ctypes.c_int(0)
         N.call("fasmg_engine_solve_wait", self.handle, hist, ctypes.byref(n))
